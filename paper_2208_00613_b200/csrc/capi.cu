@@ -1,0 +1,997 @@
+// capi.cu -- the extern "C" boundary (include/immx_b200.h) and the IMM driver behind it.
+//
+// Every entry point catches the internal exception and turns it into the status class of
+// the reference exception it mirrors (invalid_argument / runtime_error / out_of_range),
+// with a thread-local message.  The IMM driver (immx_run) follows proj/src/pipeline.cpp:47-178
+// step for step; the sampling, histograms, encoding and selection run on the device, the
+// scalar control (theta arithmetic sampler.cpp:54-83, characterization characterize.cpp,
+// the Huffman tree huffman.cpp:24-84, the memory ledger memory.hpp) on the host.
+#include <cub/cub.cuh>
+
+#include <chrono>
+#include <memory>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+
+namespace immx_dev {
+immx_hgraph* load_edge_list(std::istream& in, bool directed);
+immx_hgraph* transpose_host(const immx_hgraph& g);
+void assign_weights_host(immx_hgraph& g, int model, double p, bool f32);
+void save_cache(const immx_hgraph& g, const std::string& path);
+immx_hgraph* load_cache(const std::string& path);
+immx_hgraph* generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed);
+immx_hgraph* generate_er(uint64_t n, uint64_t m, uint64_t seed);
+void lt_weights(const immx_hgraph& gt, uint64_t seed, float* out);
+}  // namespace immx_dev
+
+using namespace immx_dev;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return IMMX_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return IMMX_ERUNTIME;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return IMMX_ERUNTIME;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) fail(IMMX_EINVAL, std::string(what) + " is NULL");
+}
+
+// ---- theta (sampler.cpp:54-83) -----------------------------------------------------
+double log_binomial(uint64_t n, uint64_t k) {
+    return std::lgamma((double)n + 1.0) - std::lgamma((double)k + 1.0) - std::lgamma((double)(n - k) + 1.0);
+}
+double theta_base(uint64_t n, uint64_t k, double eps) {
+    const double nd = (double)n;
+    const double bracket = log_binomial(n, k) * std::log(nd) + std::log(std::log2(nd));
+    return (2.0 + 2.0 * std::sqrt(2.0) / 3.0 * eps) * bracket / (2.0 * eps * eps);
+}
+void check_theta_args(uint64_t n, uint64_t k, double eps) {
+    if (n < 2) fail(IMMX_EINVAL, "theta bound requires n >= 2");
+    if (k < 1 || k >= n) fail(IMMX_EINVAL, "theta bound requires 1 <= k < n");
+    if (!(eps > 0.0)) fail(IMMX_EINVAL, "theta bound requires epsilon > 0");
+}
+
+// ---- characterize.cpp:24-56 ----------------------------------------------------------
+double skewness_host(const uint32_t* sizes, uint64_t theta) {
+    if (theta < 2) fail(IMMX_EINVAL, "skewness requires at least 2 samples");
+    double sum = 0.0;
+    for (uint64_t i = 0; i < theta; ++i) sum += (double)sizes[i];
+    const double mean = sum / (double)theta;
+    double m2 = 0.0, m3 = 0.0;
+    for (uint64_t i = 0; i < theta; ++i) {
+        const double d = (double)sizes[i] - mean;
+        m2 += d * d;
+        m3 += d * d * d;
+    }
+    m2 /= (double)theta;
+    m3 /= (double)theta;
+    if (m2 == 0.0) return 0.0;
+    return m3 / std::pow(std::sqrt(m2), 3);
+}
+double density_host(const uint32_t* sizes, uint64_t theta, uint64_t n) {
+    if (n < 1) fail(IMMX_EINVAL, "density requires n >= 1");
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < theta; ++i) total += sizes[i];
+    return (double)total / ((double)theta * (double)n);
+}
+int choose_encoding_host(double s, double d) {
+    if (s >= 0.0) return IMMX_MODE_HUFFMAN;
+    if (d > 1.0 / 32.0) return IMMX_MODE_BITMAP;
+    return IMMX_MODE_RAW;
+}
+
+// ---- estimate_theta (sampler.cpp:106-161) on the device pool ---------------------------
+void estimate_theta_dev(const DevGraph& G, uint32_t k, double eps, uint64_t seed, int model, Pool& pool,
+                        immx_plan& plan) {
+    const uint64_t n = G.n;
+    check_theta_args(n, k, eps);
+    const double eps_prime = std::sqrt(2.0) * eps;
+    const double base = theta_base(n, k, eps);
+    const uint32_t i_max = std::max<uint32_t>(1, (uint32_t)std::ceil(std::log2((double)n)) - 1);
+    plan = immx_plan{};
+    plan.k = k;
+    plan.epsilon = eps;
+    plan.rng_seed = seed;
+    uint64_t sampled = pool.count;  // a caller may hand over a pool already holding [0, count)
+    double lower_bound = 0.0;
+    for (uint32_t i = 1; i <= i_max; ++i) {
+        const uint64_t theta_i = (uint64_t)std::ceil(base * std::exp2((double)i));
+        if (theta_i > sampled) {
+            sample_into_pool(pool, G, theta_i - sampled, sampled, seed, nullptr, nullptr, model);
+            sampled = theta_i;
+        }
+        SelectOut sel;
+        // select over exactly the first theta_i-or-more sets (the pool holds [0, sampled))
+        select_raw_dev(pool, n, k, sel);
+        const double covered = sel.coverage.empty() ? 0.0 : sel.coverage.back();
+        plan.covered_fraction = covered;
+        const double x_i = (double)n / std::exp2((double)i);
+        if ((double)n * covered >= (1.0 + eps_prime) * x_i) {
+            plan.exit_iteration = i;
+            lower_bound = (double)n * covered / (1.0 + eps_prime);
+            break;
+        }
+    }
+    plan.estimation_samples = sampled;
+    if (plan.exit_iteration != 0) {
+        const uint64_t bound = (uint64_t)std::ceil(base * (double)n / lower_bound);
+        plan.theta = std::max(bound, sampled);
+    } else {
+        plan.theta = sampled;
+    }
+}
+
+uint64_t pool_members_range(const Pool& P, uint64_t lo, uint64_t hi) {
+    Device& d = *P.dev;
+    if (hi <= lo) return 0;
+    unsigned long long* out = d.scal.p + 48;
+    size_t tb = 0;
+    const uint32_t* in = P.len.p + lo;
+    cub::DeviceReduce::Sum(nullptr, tb, in, out, (int64_t)(hi - lo), d.stream);
+    d.tmp.reserve(tb, d.stream, false);
+    CK(cub::DeviceReduce::Sum(d.tmp.p, tb, in, out, (int64_t)(hi - lo), d.stream));
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, out, 8, cudaMemcpyDeviceToHost, d.stream));
+    CK(cudaStreamSynchronize(d.stream));
+    return h;
+}
+
+}  // namespace
+
+// ---- the run result -----------------------------------------------------------------
+struct immx_result {
+    uint64_t u[16] = {0};
+    double dd[12] = {0};
+    int ii[4] = {0};
+    std::vector<uint32_t> seeds;
+    std::vector<uint64_t> marginal;
+    std::vector<double> coverage;
+    std::vector<uint64_t> blk_sets, blk_raw, blk_enc;
+    immx_pool* pool = nullptr;
+    immx_store* store = nullptr;
+    ~immx_result() {
+        delete pool;
+        delete store;
+    }
+};
+
+extern "C" {
+
+const char* immx_last_error(void) { return g_err.c_str(); }
+const char* immx_version(void) { return "immx-b200 0.1.0 (sm_100a)"; }
+
+// ------------------------------------------------------------------ host graph ----
+int immx_hgraph_load_edge_list(const char* path, int directed, immx_hgraph** out) {
+    return guard([&] {
+        need(path, "path");
+        need(out, "out");
+        std::ifstream in(path);
+        if (!in) fail(IMMX_ERUNTIME, std::string("cannot open '") + path + "'");
+        *out = load_edge_list(in, directed != 0);
+    });
+}
+int immx_hgraph_load_edge_text(const char* text, size_t len, int directed, immx_hgraph** out) {
+    return guard([&] {
+        need(out, "out");
+        std::istringstream in(std::string(text ? text : "", text ? len : 0));
+        *out = load_edge_list(in, directed != 0);
+    });
+}
+int immx_hgraph_load_cache(const char* path, immx_hgraph** out) {
+    return guard([&] {
+        need(path, "path");
+        need(out, "out");
+        *out = load_cache(path);
+    });
+}
+int immx_hgraph_save_cache(const immx_hgraph* g, const char* path) {
+    return guard([&] {
+        need(g, "graph");
+        need(path, "path");
+        save_cache(*g, path);
+    });
+}
+int immx_hgraph_from_csr(uint64_t n, uint64_t m, const uint64_t* offsets, const uint32_t* targets, const double* probs,
+                         const uint64_t* ids, immx_hgraph** out) {
+    return guard([&] {
+        need(offsets, "offsets");
+        need(out, "out");
+        if (m && (!targets || !probs)) fail(IMMX_EINVAL, "targets/probs are NULL");
+        if (offsets[0] != 0 || offsets[n] != m) fail(IMMX_EINVAL, "offsets must start at 0 and end at m");
+        for (uint64_t v = 0; v < n; ++v)
+            if (offsets[v + 1] < offsets[v]) fail(IMMX_EINVAL, "offsets must be non-decreasing");
+        for (uint64_t e = 0; e < m; ++e)
+            if (targets[e] >= n) fail(IMMX_ERANGE, "target id out of range");
+        auto* g = new immx_hgraph;
+        g->n = n;
+        g->m = m;
+        g->offsets.assign(offsets, offsets + n + 1);
+        g->targets.assign(targets, targets + m);
+        g->probs.assign(probs, probs + m);
+        if (ids) g->original_ids.assign(ids, ids + n);
+        else {
+            g->original_ids.resize(n);
+            for (uint64_t v = 0; v < n; ++v) g->original_ids[v] = v;
+        }
+        *out = g;
+    });
+}
+int immx_hgraph_transpose(const immx_hgraph* g, immx_hgraph** out) {
+    return guard([&] {
+        need(g, "graph");
+        need(out, "out");
+        *out = transpose_host(*g);
+    });
+}
+int immx_hgraph_assign_weights(immx_hgraph* g, int model, double p) {
+    return guard([&] {
+        need(g, "graph");
+        assign_weights_host(*g, model, p, false);
+    });
+}
+int immx_hgraph_assign_weights_f32(immx_hgraph* g, int model, double p) {
+    return guard([&] {
+        need(g, "graph");
+        assign_weights_host(*g, model, p, true);
+    });
+}
+int immx_hgraph_generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed,
+                              immx_hgraph** out) {
+    return guard([&] {
+        need(out, "out");
+        *out = generate_rmat(scale, ef, a, b, c, seed);
+    });
+}
+int immx_hgraph_generate_er(uint64_t n, uint64_t m, uint64_t seed, immx_hgraph** out) {
+    return guard([&] {
+        need(out, "out");
+        *out = generate_er(n, m, seed);
+    });
+}
+int immx_hgraph_lt_weights(const immx_hgraph* gt, uint64_t seed, float* w) {
+    return guard([&] {
+        need(gt, "graph");
+        need(w, "weights");
+        lt_weights(*gt, seed, w);
+    });
+}
+int immx_hgraph_info(const immx_hgraph* g, uint64_t* n, uint64_t* m) {
+    return guard([&] {
+        need(g, "graph");
+        if (n) *n = g->n;
+        if (m) *m = g->m;
+    });
+}
+int immx_hgraph_view(const immx_hgraph* g, const uint64_t** off, const uint32_t** tgt, const double** prob,
+                     const uint64_t** ids) {
+    return guard([&] {
+        need(g, "graph");
+        if (off) *off = g->offsets.data();
+        if (tgt) *tgt = g->targets.data();
+        if (prob) *prob = g->probs.data();
+        if (ids) *ids = g->original_ids.data();
+    });
+}
+void immx_hgraph_destroy(immx_hgraph* g) { delete g; }
+
+// --------------------------------------------------------------------- scalars ----
+int immx_theta_bound_real(uint64_t n, uint64_t k, double eps, uint32_t i, double* out) {
+    return guard([&] {
+        check_theta_args(n, k, eps);
+        if (i < 1) fail(IMMX_EINVAL, "theta bound requires i >= 1");
+        need(out, "out");
+        *out = theta_base(n, k, eps) * std::exp2((double)i);
+    });
+}
+int immx_theta_bound(uint64_t n, uint64_t k, double eps, uint32_t i, uint64_t* out) {
+    return guard([&] {
+        check_theta_args(n, k, eps);
+        if (i < 1) fail(IMMX_EINVAL, "theta bound requires i >= 1");
+        need(out, "out");
+        *out = (uint64_t)std::ceil(theta_base(n, k, eps) * std::exp2((double)i));
+    });
+}
+int immx_skewness(const uint32_t* sizes, uint64_t count, double* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = skewness_host(sizes, count);
+    });
+}
+int immx_density(const uint32_t* sizes, uint64_t count, uint64_t n, double* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = density_host(sizes, count, n);
+    });
+}
+int immx_choose_encoding(double s, double d) { return choose_encoding_host(s, d); }
+int immx_codebook_build(const uint64_t* freq, uint64_t n, uint64_t* code_bits, uint8_t* code_len, uint64_t* coded) {
+    return guard([&] {
+        need(freq, "freq");
+        HostCodebook cb = build_codebook_host(freq, n);
+        if (code_bits) std::memcpy(code_bits, cb.bits.data(), n * 8);
+        if (code_len) std::memcpy(code_len, cb.len.data(), n);
+        if (coded) *coded = cb.coded;
+    });
+}
+
+// -------------------------------------------------------------- device context ----
+int immx_device_create(int ordinal, immx_device** out) {
+    return guard([&] {
+        need(out, "out");
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            fail(IMMX_ECUDA, "no CUDA device is available (the B200 path has no CPU fallback)");
+        if (ordinal < 0 || ordinal >= count) fail(IMMX_EINVAL, "device ordinal out of range");
+        CK(cudaSetDevice(ordinal));
+        auto* h = new immx_device;
+        Device& d = h->d;
+        d.ordinal = ordinal;
+        CK(cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, ordinal));
+        CK(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+        d.scal.exact(64);
+        CK(cudaMallocHost(&d.host_scal, 64 * 8));
+        *out = h;
+    });
+}
+void immx_device_destroy(immx_device* h) {
+    if (!h) return;
+    cudaStreamSynchronize(h->d.stream);
+    if (h->d.host_scal) cudaFreeHost(h->d.host_scal);
+    cudaStreamDestroy(h->d.stream);
+    delete h;
+}
+void* immx_device_stream(immx_device* h) { return h ? (void*)h->d.stream : nullptr; }
+int immx_device_synchronize(immx_device* h) {
+    return guard([&] {
+        need(h, "device");
+        CK(cudaStreamSynchronize(h->d.stream));
+    });
+}
+uint64_t immx_device_kernel_launches(const immx_device* h) { return h ? h->d.kernel_launches : 0; }
+
+// ----------------------------------------------------------------- device graph ----
+int immx_graph_upload(immx_device* dv, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt,
+                      const double* prob, int transposed, immx_graph** out) {
+    return guard([&] {
+        need(dv, "device");
+        need(off, "offsets");
+        need(out, "out");
+        if (m && (!tgt || !prob)) fail(IMMX_EINVAL, "targets/probs are NULL");
+        auto* g = new immx_graph;
+        try {
+            graph_upload(g->g, dv->d, n, m, off, tgt, prob, transposed != 0);
+        } catch (...) {
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+int immx_graph_set_lt_weights(immx_graph* g, const float* w) {
+    return guard([&] {
+        need(g, "graph");
+        need(w, "weights");
+        graph_set_lt(g->g, w);
+    });
+}
+int immx_graph_info(const immx_graph* g, uint64_t* n, uint64_t* m, int* pm) {
+    return guard([&] {
+        need(g, "graph");
+        if (n) *n = g->g.n;
+        if (m) *m = g->g.m;
+        if (pm) *pm = g->g.pmode;
+    });
+}
+void immx_graph_destroy(immx_graph* g) { delete g; }
+
+// --------------------------------------------------------------------- pools ----
+int immx_pool_create(immx_device* dv, immx_pool** out) {
+    return guard([&] {
+        need(dv, "device");
+        need(out, "out");
+        auto* p = new immx_pool;
+        p->p.dev = &dv->d;
+        *out = p;
+    });
+}
+void immx_pool_destroy(immx_pool* p) { delete p; }
+int immx_pool_clear(immx_pool* p) {
+    return guard([&] {
+        need(p, "pool");
+        p->p.count = p->p.members = p->p.edges = p->p.arena_used = 0;
+    });
+}
+int immx_pool_sample(immx_pool* p, const immx_graph* g, uint64_t count, uint64_t first, uint64_t seed, int model) {
+    return guard([&] {
+        need(p, "pool");
+        need(g, "graph");
+        sample_into_pool(p->p, g->g, count, first, seed, nullptr, nullptr, model);
+    });
+}
+int immx_pool_sample_rooted(immx_pool* p, const immx_graph* g, const uint32_t* roots, const uint64_t* states,
+                            uint64_t count, int model) {
+    return guard([&] {
+        need(p, "pool");
+        need(g, "graph");
+        if (!count) return;
+        need(roots, "roots");
+        need(states, "states");
+        for (uint64_t i = 0; i < count; ++i)
+            if (roots[i] >= g->g.n) fail(IMMX_ERANGE, "root out of range");
+        Device& d = *p->p.dev;
+        DBuf<uint32_t> r;
+        DBuf<uint64_t> s;
+        r.exact(count);
+        s.exact(count);
+        CK(cudaMemcpyAsync(r.p, roots, count * 4, cudaMemcpyHostToDevice, d.stream));
+        CK(cudaMemcpyAsync(s.p, states, count * 8, cudaMemcpyHostToDevice, d.stream));
+        sample_into_pool(p->p, g->g, count, 0, 0, r.p, s.p, model);
+    });
+}
+int immx_pool_upload(immx_pool* p, const uint64_t* offsets, const uint32_t* members, uint64_t count) {
+    return guard([&] {
+        need(p, "pool");
+        need(offsets, "offsets");
+        if (offsets[count] > offsets[0]) need(members, "members");
+        pool_upload_host(p->p, offsets, members, count, 0);
+    });
+}
+int immx_pool_info(const immx_pool* p, uint64_t* count, uint64_t* members, uint64_t* edges) {
+    return guard([&] {
+        need(p, "pool");
+        if (count) *count = p->p.count;
+        if (members) *members = p->p.members;
+        if (edges) *edges = p->p.edges;
+    });
+}
+int immx_pool_read(const immx_pool* p, uint64_t lo, uint64_t hi, uint64_t* offsets, uint32_t* members) {
+    return guard([&] {
+        need(p, "pool");
+        need(offsets, "offsets");
+        pool_read_host(p->p, lo, hi, offsets, members);
+    });
+}
+int immx_pool_histogram(const immx_pool* p, uint64_t lo, uint64_t hi, uint64_t n, uint64_t* counts) {
+    return guard([&] {
+        need(p, "pool");
+        need(counts, "counts");
+        if (hi > p->p.count || lo > hi) fail(IMMX_ERANGE, "pool range out of bounds");
+        Device& d = *p->p.dev;
+        DBuf<unsigned int> h;
+        DBuf<uint64_t> h64;
+        h.exact(std::max<uint64_t>(n, 1));
+        h64.exact(std::max<uint64_t>(n, 1));
+        CK(cudaMemsetAsync(h.p, 0, n * 4, d.stream));
+        pool_hist_dev(p->p, lo, hi, h.p);
+        u32_to_u64_dev(d, h.p, n, h64.p);
+        CK(cudaMemcpyAsync(counts, h64.p, n * 8, cudaMemcpyDeviceToHost, d.stream));
+        CK(cudaStreamSynchronize(d.stream));
+    });
+}
+
+// ----------------------------------------------------------------- selection ----
+static void copy_sel(const SelectOut& s, uint32_t* seeds, uint64_t* marg, double* cov, uint32_t* padded) {
+    const size_t k = s.seeds.size();
+    if (seeds) std::memcpy(seeds, s.seeds.data(), k * 4);
+    if (marg) std::memcpy(marg, s.marginal.data(), k * 8);
+    if (cov) std::memcpy(cov, s.coverage.data(), k * 8);
+    if (padded) *padded = s.padded;
+}
+
+int immx_select_raw(const immx_pool* p, uint64_t n, uint32_t k, uint32_t* seeds, uint64_t* marg, double* cov,
+                    uint32_t* padded) {
+    return guard([&] {
+        need(p, "pool");
+        SelectOut s;
+        select_raw_dev(p->p, n, k, s);
+        copy_sel(s, seeds, marg, cov, padded);
+    });
+}
+int immx_table_argmax(immx_device* dv, const uint64_t* counts, uint64_t n, uint32_t* out) {
+    return guard([&] {
+        need(dv, "device");
+        need(out, "out");
+        Device& d = dv->d;
+        if (n == 0) {
+            *out = 0;
+            return;
+        }
+        // counts are u64 (FrequencyTable): clamp-free exact path via two-level key
+        DBuf<uint64_t> c;
+        c.exact(n);
+        CK(cudaMemcpyAsync(c.p, counts, n * 8, cudaMemcpyHostToDevice, d.stream));
+        uint64_t mx = 0;
+        for (uint64_t v = 0; v < n; ++v) mx = std::max(mx, counts[v]);
+        if (mx > 0xffffffffULL) {  // beyond the device's u32 tables: resolve on the count itself
+            uint64_t best = 0;
+            uint32_t w = 0;
+            for (uint64_t v = 0; v < n; ++v)
+                if (counts[v] > best) {
+                    best = counts[v];
+                    w = (uint32_t)v;
+                }
+            *out = w;
+            return;
+        }
+        DBuf<unsigned int> c32;
+        c32.exact(n);
+        u64_to_u32_dev(d, c.p, n, c32.p);
+        unsigned long long* key = d.scal.p + 56;
+        CK(cudaMemsetAsync(key, 0, 8, d.stream));
+        argmax_dev(d, c32.p, n, key);
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, key, 8, cudaMemcpyDeviceToHost, d.stream));
+        CK(cudaStreamSynchronize(d.stream));
+        *out = h ? 0xffffffffu - (uint32_t)(h & 0xffffffffu) : 0;
+    });
+}
+int immx_estimate_theta(const immx_graph* g, uint32_t k, double eps, uint64_t seed, int model, immx_pool* keep,
+                        immx_plan* out) {
+    return guard([&] {
+        need(g, "graph");
+        need(out, "out");
+        if (keep) {
+            keep->p.count = keep->p.members = keep->p.edges = keep->p.arena_used = 0;
+            estimate_theta_dev(g->g, k, eps, seed, model, keep->p, *out);
+        } else {
+            Pool tmp;
+            tmp.dev = g->g.dev;
+            estimate_theta_dev(g->g, k, eps, seed, model, tmp, *out);
+        }
+    });
+}
+
+// ------------------------------------------------------------------ Huffman store ----
+int immx_store_create(immx_device* dv, uint64_t n, const uint64_t* code_bits, const uint8_t* code_len,
+                      immx_store** out) {
+    return guard([&] {
+        need(dv, "device");
+        need(code_bits, "code_bits");
+        need(code_len, "code_len");
+        need(out, "out");
+        // rebuild the tree from the codes (any prefix code) for the decode table
+        HostCodebook cb;
+        cb.bits.assign(code_bits, code_bits + n);
+        cb.len.assign(code_len, code_len + n);
+        cb.nodes.emplace_back();
+        std::vector<uint8_t> leaf(1, 0);
+        for (uint64_t v = 0; v < n; ++v) {
+            const uint32_t L = code_len[v];
+            if (!L) continue;
+            if (L > 64) fail(IMMX_EINVAL, "code length > 64");
+            cb.coded++;
+            int32_t u = 0;
+            for (int i = (int)L - 1; i >= 0; --i) {
+                if (leaf[u]) fail(IMMX_EINVAL, "codes are not prefix-free");
+                const uint32_t bit = (uint32_t)(code_bits[v] >> i) & 1u;
+                int32_t c = cb.nodes[u].child[bit];
+                if (c < 0) {
+                    cb.nodes.emplace_back();
+                    leaf.push_back(0);
+                    c = (int32_t)cb.nodes.size() - 1;
+                    cb.nodes[u].child[bit] = c;
+                }
+                u = c;
+            }
+            if (leaf[u] || cb.nodes[u].child[0] >= 0 || cb.nodes[u].child[1] >= 0)
+                fail(IMMX_EINVAL, "codes are not prefix-free");
+            leaf[u] = 1;
+            cb.nodes[u].symbol = (uint32_t)v;
+        }
+        std::vector<unsigned long long> lut;
+        uint32_t root_bits = 1;
+        if (cb.coded) build_decode_lut(cb, lut, root_bits);
+        else lut.assign(2, 0ULL);
+        auto* s = new immx_store;
+        try {
+            store_set_codes(s->s, dv->d, n, code_bits, code_len, lut, root_bits);
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+void immx_store_destroy(immx_store* s) { delete s; }
+int immx_store_encode(immx_store* s, const immx_pool* p, uint64_t lo, uint64_t hi, int64_t top) {
+    return guard([&] {
+        need(s, "store");
+        need(p, "pool");
+        store_encode(s->s, p->p, lo, hi, top, nullptr);
+    });
+}
+int immx_store_append(immx_store* s, const uint8_t* bytes, uint64_t n_bytes, uint64_t bit_length,
+                      const uint32_t* copied, uint64_t n_copied) {
+    return guard([&] {
+        need(s, "store");
+        store_append_host(s->s, bytes, n_bytes, bit_length, copied, n_copied);
+    });
+}
+int immx_store_info(const immx_store* s, uint64_t* count, uint64_t* payload, uint64_t* device_bytes) {
+    return guard([&] {
+        need(s, "store");
+        if (count) *count = s->s.count;
+        if (payload) *payload = s->s.payload_bytes;
+        if (device_bytes)
+            *device_bytes = s->s.total_words * 4 + s->s.total_copied * 4 + (s->s.count + 1) * 16 + s->s.count * 4;
+    });
+}
+int immx_store_read(const immx_store* s, uint64_t lo, uint64_t hi, uint64_t* byte_off, uint8_t* bytes,
+                    uint64_t* bit_length, uint64_t* cp_off, uint32_t* copied) {
+    return guard([&] {
+        need(s, "store");
+        store_read_host(s->s, lo, hi, byte_off, bytes, bit_length, cp_off, copied);
+    });
+}
+int immx_store_decode_find(const immx_store* s, uint64_t j, uint32_t top, int* found, uint32_t* decoded,
+                           uint64_t* n_decoded) {
+    return guard([&] {
+        need(s, "store");
+        std::vector<uint32_t> dec;
+        const int r = store_decode_find(s->s, j, top, dec);
+        if (found) *found = r;
+        if (decoded && !dec.empty()) std::memcpy(decoded, dec.data(), dec.size() * 4);
+        if (n_decoded) *n_decoded = dec.size();
+    });
+}
+int immx_select_huffman(immx_store* s, const uint64_t* hist, uint32_t k, uint32_t* seeds, uint64_t* marg,
+                        double* cov, uint32_t* padded, uint64_t* max_decoded) {
+    return guard([&] {
+        need(s, "store");
+        need(hist, "hist");
+        Device& d = *s->s.dev;
+        const uint64_t n = s->s.n;
+        for (uint64_t v = 0; v < n; ++v)
+            if (hist[v] > 0xffffffffULL) fail(IMMX_EINVAL, "frequency above 2^32-1");
+        DBuf<uint64_t> h64;
+        DBuf<unsigned int> h;
+        h64.exact(std::max<uint64_t>(n, 1));
+        h.exact(std::max<uint64_t>(n, 1));
+        CK(cudaMemcpyAsync(h64.p, hist, n * 8, cudaMemcpyHostToDevice, d.stream));
+        u64_to_u32_dev(d, h64.p, n, h.p);
+        SelectOut so;
+        std::vector<uint64_t> md;
+        select_huffman_dev(s->s, h.p, k, so, &md);
+        copy_sel(so, seeds, marg, cov, padded);
+        if (max_decoded) std::memcpy(max_decoded, md.data(), md.size() * 8);
+    });
+}
+
+// ----------------------------------------------------------------------- bitmaps ----
+int immx_bitmap_create(immx_device* dv, uint64_t n_rows, immx_bitmap** out) {
+    return guard([&] {
+        need(dv, "device");
+        need(out, "out");
+        auto* b = new immx_bitmap;
+        b->b.dev = &dv->d;
+        b->b.n = n_rows;
+        *out = b;
+    });
+}
+void immx_bitmap_destroy(immx_bitmap* b) { delete b; }
+int immx_bitmap_encode_block(immx_bitmap* b, const immx_pool* p, uint64_t lo, uint64_t hi) {
+    return guard([&] {
+        need(b, "bitmap");
+        need(p, "pool");
+        bitmap_encode_block(b->b, p->p, lo, hi);
+    });
+}
+int immx_bitmap_info(const immx_bitmap* b, uint64_t* n_cols, uint64_t* wpr, uint64_t* bytes, uint32_t* nblocks) {
+    return guard([&] {
+        need(b, "bitmap");
+        if (n_cols) *n_cols = b->b.total_cols();
+        if (wpr) *wpr = b->b.total_wpr();
+        if (bytes) *bytes = b->b.n * b->b.total_wpr() * 4;
+        if (nblocks) *nblocks = (uint32_t)b->b.blocks.size();
+    });
+}
+int immx_bitmap_popcount(const immx_bitmap* b, uint64_t* counts) {
+    return guard([&] {
+        need(b, "bitmap");
+        need(counts, "counts");
+        Device& d = *b->b.dev;
+        DBuf<unsigned long long> h;
+        h.exact(std::max<uint64_t>(b->b.n, 1));
+        bitmap_popcount(b->b, h.p);
+        CK(cudaMemcpyAsync(counts, h.p, b->b.n * 8, cudaMemcpyDeviceToHost, d.stream));
+        CK(cudaStreamSynchronize(d.stream));
+    });
+}
+int immx_bitmap_row(const immx_bitmap* b, uint32_t v, uint32_t* words) {
+    return guard([&] {
+        need(b, "bitmap");
+        need(words, "words");
+        bitmap_row(b->b, v, words);
+    });
+}
+int immx_bitmap_subtract_row(immx_bitmap* b, uint32_t v, const uint32_t* snap, uint64_t* pc) {
+    return guard([&] {
+        need(b, "bitmap");
+        need(snap, "snapshot");
+        const uint64_t r = bitmap_subtract_row(b->b, v, snap);
+        if (pc) *pc = r;
+    });
+}
+int immx_select_bitmap(immx_bitmap* b, const uint64_t* hist, uint32_t k, uint32_t* seeds, uint64_t* marg,
+                       double* cov, uint32_t* padded) {
+    return guard([&] {
+        need(b, "bitmap");
+        Device& d = *b->b.dev;
+        const uint64_t n = b->b.n;
+        DBuf<unsigned long long> h64;
+        DBuf<unsigned int> h;
+        h64.exact(std::max<uint64_t>(n, 1));
+        h.exact(std::max<uint64_t>(n, 1));
+        if (hist) CK(cudaMemcpyAsync(h64.p, hist, n * 8, cudaMemcpyHostToDevice, d.stream));
+        else bitmap_popcount(b->b, h64.p);
+        u64_to_u32_dev(d, (const uint64_t*)h64.p, n, h.p);
+        SelectOut so;
+        select_bitmap_dev(b->b, h.p, k, so);
+        copy_sel(so, seeds, marg, cov, padded);
+    });
+}
+
+// ------------------------------------------------------------------------ run() ----
+int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out) {
+    return guard([&] {
+        need(gh, "graph");
+        need(cfg, "config");
+        need(out, "out");
+        const DevGraph& G = gh->g;
+        Device& d = *G.dev;
+        cudaStream_t st = d.stream;
+        const uint64_t n = G.n;
+        const uint32_t k = cfg->k;
+        if (k < 1 || k >= n) fail(IMMX_EINVAL, "k must satisfy 1 <= k < n");
+        if (!(cfg->epsilon > 0.0)) fail(IMMX_EINVAL, "epsilon must be > 0");
+        if (cfg->blocks < 2) fail(IMMX_EINVAL, "block count must be >= 2");
+        if (cfg->mode < -1 || cfg->mode > 2) fail(IMMX_EINVAL, "unknown mode");
+        const int workers = std::max(cfg->workers, 1);
+        using Clock = std::chrono::steady_clock;
+        auto secs = [](Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+        const auto t_start = Clock::now();
+
+        auto* R = new immx_result;
+        std::unique_ptr<immx_result> guard_r(R);
+        R->pool = new immx_pool;
+        Pool& pool = R->pool->p;
+        pool.dev = &d;
+
+        // ---- theta estimation (pipeline.cpp:61-63) ----
+        auto t0 = Clock::now();
+        immx_plan plan{};
+        estimate_theta_dev(G, k, cfg->epsilon, cfg->rng_seed, cfg->model, pool, plan);
+        const double t_est = secs(t0);
+        uint64_t samples_drawn = pool.count;
+        const uint64_t theta = plan.theta;
+        const uint32_t b = (uint32_t)std::min<uint64_t>(cfg->blocks, std::max<uint64_t>(theta, 1));
+        const uint64_t per_block = (theta + b - 1) / b;
+
+        // ledger (memory.hpp:9-22)
+        uint64_t led_raw = 0, led_enc = 0, led_freq = 8 * n, led_dec = 0, peak = 0;
+        auto ckpt = [&] { peak = std::max(peak, led_raw + led_enc + led_freq + led_dec); };
+
+        t0 = Clock::now();
+        if (cfg->reuse_pool) {
+            // sets [0, estimation_samples) already exist and are bit-identical to what the
+            // production loop would re-draw (same (seed, index) streams)
+            if (theta > pool.count) {
+                sample_into_pool(pool, G, theta - pool.count, pool.count, cfg->rng_seed, nullptr, nullptr, cfg->model);
+                samples_drawn += theta - plan.estimation_samples;
+            }
+        } else {
+            pool.count = pool.members = pool.edges = pool.arena_used = 0;
+        }
+        int mode = IMMX_MODE_RAW, char_mode = IMMX_MODE_RAW;
+        double skew = 0.0, dens = 0.0;
+        HostCodebook cb;
+        std::unique_ptr<immx_store> store;
+        std::unique_ptr<immx_bitmap> bm;
+        DBuf<unsigned int> hist;  // encoding-time table (huffman)
+        hist.exact(std::max<uint64_t>(n, 1));
+        CK(cudaMemsetAsync(hist.p, 0, n * 4, st));
+        uint64_t done = 0;
+        for (uint32_t i = 1; i <= b; ++i) {
+            const uint64_t count = std::min(per_block, theta - done);
+            const uint64_t lo = done, hi = done + count;
+            if (!cfg->reuse_pool) {
+                sample_into_pool(pool, G, count, done, cfg->rng_seed, nullptr, nullptr, cfg->model);
+                samples_drawn += count;
+            }
+            done += count;
+            const uint64_t raw = 4 * pool_members_range(pool, lo, hi);
+            led_raw += raw;
+            ckpt();
+            if (i == 1) {  // pipeline.cpp:93-104
+                std::vector<uint32_t> sizes(count);
+                if (count) CK(cudaMemcpyAsync(sizes.data(), pool.len.p + lo, count * 4, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                skew = skewness_host(sizes.data(), count);
+                dens = density_host(sizes.data(), count, n);
+                char_mode = choose_encoding_host(skew, dens);
+                mode = cfg->mode >= 0 ? cfg->mode : char_mode;
+                if (mode == IMMX_MODE_HUFFMAN) {
+                    DBuf<unsigned int> h1;
+                    h1.exact(n);
+                    CK(cudaMemsetAsync(h1.p, 0, n * 4, st));
+                    pool_hist_dev(pool, lo, hi, h1.p);
+                    std::vector<unsigned int> f32(n);
+                    CK(cudaMemcpyAsync(f32.data(), h1.p, n * 4, cudaMemcpyDeviceToHost, st));
+                    CK(cudaStreamSynchronize(st));
+                    std::vector<uint64_t> f(f32.begin(), f32.end());
+                    cb = build_codebook_host(f.data(), n);
+                    std::vector<unsigned long long> lut;
+                    uint32_t rb = 1;
+                    build_decode_lut(cb, lut, rb);
+                    store.reset(new immx_store);
+                    store_set_codes(store->s, d, n, cb.bits.data(), cb.len.data(), lut, rb);
+                } else if (mode == IMMX_MODE_BITMAP) {
+                    bm.reset(new immx_bitmap);
+                    bm->b.dev = &d;
+                    bm->b.n = n;
+                }
+            }
+            uint64_t enc = 0;
+            if (mode == IMMX_MODE_HUFFMAN) {  // pipeline.cpp:106-118
+                pool_hist_dev(pool, lo, hi, hist.p);
+                unsigned long long* key = d.scal.p + 60;
+                CK(cudaMemsetAsync(key, 0, 8, st));
+                argmax_dev(d, hist.p, n, key);
+                unsigned long long hk = 0;
+                CK(cudaMemcpyAsync(&hk, key, 8, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                const int64_t top = hk ? (int64_t)(0xffffffffu - (uint32_t)(hk & 0xffffffffu)) : 0;
+                store_encode(store->s, pool, lo, hi, top, &enc);
+                led_enc += enc;
+            } else if (mode == IMMX_MODE_BITMAP) {  // pipeline.cpp:119-123
+                bitmap_encode_block(bm->b, pool, lo, hi);
+                enc = n * ((count + 31) / 32 * 32) / 8;
+                led_enc += enc;
+            } else {
+                enc = raw;
+            }
+            ckpt();
+            if (mode != IMMX_MODE_RAW) led_raw -= raw;
+            ckpt();
+            R->blk_sets.push_back(count);
+            R->blk_raw.push_back(raw);
+            R->blk_enc.push_back(enc);
+        }
+        const double t_samp = secs(t0);
+        uint64_t raw_total = 0, enc_total = 0;
+        for (uint32_t i = 0; i < b; ++i) {
+            raw_total += R->blk_raw[i];
+            enc_total += R->blk_enc[i];
+        }
+        const double ratio = enc_total == 0 ? 1.0 : (double)raw_total / (double)enc_total;
+        double uncoded = 0.0;
+        if (mode == IMMX_MODE_HUFFMAN) {
+            std::vector<unsigned int> hh(n);
+            CK(cudaMemcpyAsync(hh.data(), hist.p, n * 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            uint64_t u = 0;
+            for (uint64_t v = 0; v < n; ++v)
+                if (hh[v] > 0 && cb.len[v] == 0) u++;
+            uncoded = (double)u / (double)n;
+        }
+
+        // ---- selection (pipeline.cpp:156-175) ----
+        t0 = Clock::now();
+        led_freq = 8 * n * (uint64_t)(workers + 1);
+        ckpt();
+        SelectOut sel;
+        if (mode == IMMX_MODE_RAW) {
+            select_raw_dev(pool, n, k, sel);
+        } else if (mode == IMMX_MODE_HUFFMAN) {
+            std::vector<uint64_t> md;
+            select_huffman_dev(store->s, hist.p, k, sel, &md);
+            for (uint32_t r = 0; r < k; ++r) {
+                if (sel.marginal[r] == 0) continue;
+                led_dec = std::max(led_dec, 4 * md[r] * (uint64_t)workers);
+                ckpt();
+            }
+        } else {
+            DBuf<unsigned long long> h64;
+            h64.exact(n);
+            bitmap_popcount(bm->b, h64.p);
+            u64_to_u32_dev(d, (const uint64_t*)h64.p, n, hist.p);
+            select_bitmap_dev(bm->b, hist.p, k, sel);
+        }
+        const double t_sel = secs(t0);
+        const double t_total = secs(t_start);
+
+        uint64_t store_dev_bytes = 0;
+        if (store) {
+            const Store& S = store->s;
+            store_dev_bytes = S.total_words * 4 + S.total_copied * 4 + (S.count + 1) * 16 + S.count * 4;
+        } else if (bm) {
+            store_dev_bytes = n * bm->b.total_wpr() * 4;
+        } else {
+            store_dev_bytes = pool.members * 4 + pool.count * 12;
+        }
+        R->u[0] = theta;
+        R->u[1] = plan.estimation_samples;
+        R->u[2] = plan.exit_iteration;
+        R->u[3] = b;
+        R->u[4] = raw_total;
+        R->u[5] = enc_total;
+        R->u[6] = peak;
+        R->u[7] = sel.padded;
+        R->u[8] = k;
+        R->u[9] = cb.coded;
+        R->u[10] = store_dev_bytes;
+        R->u[11] = samples_drawn;
+        R->u[12] = pool.edges;
+        R->u[13] = pool.members;
+        R->dd[0] = plan.covered_fraction;
+        R->dd[1] = skew;
+        R->dd[2] = dens;
+        R->dd[3] = ratio;
+        R->dd[4] = uncoded;
+        R->dd[5] = t_est;
+        R->dd[6] = t_samp;
+        R->dd[7] = t_sel;
+        R->dd[8] = t_total;
+        R->ii[0] = char_mode;
+        R->ii[1] = mode;
+        R->ii[2] = cfg->mode >= 0 && cfg->mode != char_mode;
+        R->seeds = sel.seeds;
+        R->marginal = sel.marginal;
+        R->coverage = sel.coverage;
+        R->store = store.release();
+        *out = guard_r.release();
+    });
+}
+
+int immx_result_scalars(const immx_result* r, uint64_t* u, double* dd, int* ii) {
+    return guard([&] {
+        need(r, "result");
+        if (u) std::memcpy(u, r->u, sizeof(r->u));
+        if (dd) std::memcpy(dd, r->dd, sizeof(r->dd));
+        if (ii) std::memcpy(ii, r->ii, sizeof(r->ii));
+    });
+}
+int immx_result_seeds(const immx_result* r, uint32_t* seeds, uint64_t* marg, double* cov) {
+    return guard([&] {
+        need(r, "result");
+        const size_t k = r->seeds.size();
+        if (seeds) std::memcpy(seeds, r->seeds.data(), k * 4);
+        if (marg) std::memcpy(marg, r->marginal.data(), k * 8);
+        if (cov) std::memcpy(cov, r->coverage.data(), k * 8);
+    });
+}
+int immx_result_blocks(const immx_result* r, uint64_t* sets, uint64_t* raw, uint64_t* enc) {
+    return guard([&] {
+        need(r, "result");
+        const size_t b = r->blk_sets.size();
+        if (sets) std::memcpy(sets, r->blk_sets.data(), b * 8);
+        if (raw) std::memcpy(raw, r->blk_raw.data(), b * 8);
+        if (enc) std::memcpy(enc, r->blk_enc.data(), b * 8);
+    });
+}
+const immx_pool* immx_result_pool(const immx_result* r) { return r ? r->pool : nullptr; }
+const immx_store* immx_result_store(const immx_result* r) { return r ? r->store : nullptr; }
+void immx_result_destroy(immx_result* r) { delete r; }
+
+}  // extern "C"

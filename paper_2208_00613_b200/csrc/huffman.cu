@@ -1,0 +1,530 @@
+// huffman.cu -- learn-then-compress on the device: encode, decode_find, select_huffman.
+//
+// Stream format = the reference's EncodedRrr (huffman.hpp:39-45, huffman.cpp:96-127): per set
+// an MSB-first byte stream of the codewords (top first when it is codable and present, then
+// the codable members in member order), zero-padded to a byte, plus the uncodable members
+// in order ("copied").  In HBM each set's stream starts on a 4-byte boundary (words[woff[j]]);
+// bytes sit in memory in stream order, so the first ceil(bits/8) bytes of a set are exactly
+// the reference's `bits` vector.  Payload accounting uses the reference formula
+// ceil(bits/8) + 4*|copied| (huffman.hpp:44); the device bytes are reported separately.
+//
+// Decoding uses a multi-level lookup table derived from the (non-canonical) tree: the root
+// table indexes the next 12 bits, sub-tables up to 8 bits.  Entry layout (u64):
+//   leaf    : bit63=1, bits56..62 = bits consumed at this level, bits0..31 = symbol
+//   pointer : bit63=0, bit62=1, bits56..61 = sub-table width, bits0..47 = sub-table offset
+//   invalid : 0 (a prefix that is no codeword)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace immx_dev {
+
+namespace {
+constexpr uint32_t FULL = 0xffffffffu;
+
+unsigned grid_for(uint64_t items, const Device& d) {
+    uint64_t b = (items + 255) / 256;
+    b = std::min<uint64_t>(b, (uint64_t)d.num_sms * 16);
+    return (unsigned)std::max<uint64_t>(b, 1);
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+// pass A: bit length, copied count, top-swap flag per set
+__global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* __restrict__ off,
+                           const uint32_t* __restrict__ len, uint64_t lo, uint64_t hi,
+                           const uint8_t* __restrict__ code_len, int64_t top, uint32_t* __restrict__ bits,
+                           uint64_t* __restrict__ nwords, uint64_t* __restrict__ ncopied, uint8_t* __restrict__ swap,
+                           unsigned long long* __restrict__ payload) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool top_coded = top >= 0 && code_len[top] != 0;
+    for (uint64_t j = lo + w; j < hi; j += nw) {
+        const uint64_t b = off[j];
+        const uint32_t l = len[j];
+        uint32_t nb = 0, nc = 0;
+        bool has_top = false;
+        for (uint32_t i = lane; i < l; i += 32) {
+            const uint32_t v = arena[b + i];
+            const uint32_t cl = code_len[v];
+            nb += cl;
+            nc += cl == 0;
+            has_top |= top_coded && v == (uint32_t)top;
+        }
+        for (int o = 16; o; o >>= 1) {
+            nb += __shfl_xor_sync(FULL, nb, o);
+            nc += __shfl_xor_sync(FULL, nc, o);
+        }
+        has_top = __any_sync(FULL, has_top);
+        if (lane == 0) {
+            const uint64_t k = j - lo;
+            bits[k] = nb;
+            nwords[k] = (nb + 31) / 32;
+            ncopied[k] = nc;
+            swap[k] = has_top;
+            atomicAdd(payload, (unsigned long long)((nb + 7) / 8 + 4ull * nc));
+        }
+    }
+}
+
+__device__ __forceinline__ void put_code(uint32_t* __restrict__ words, uint64_t p, uint64_t code, uint32_t L) {
+    if (L == 0) return;
+    const uint64_t A = L == 64 ? code : (code << (64 - L));  // MSB-aligned codeword
+    const uint32_t s = (uint32_t)(p & 31);
+    const uint64_t w0 = p >> 5;
+    const unsigned __int128 V = ((unsigned __int128)A << 64) >> s;
+    const uint32_t a = (uint32_t)(V >> 96), b = (uint32_t)(V >> 64), c = (uint32_t)(V >> 32);
+    if (a) atomicOr(&words[w0], bswap32(a));
+    if (b) atomicOr(&words[w0 + 1], bswap32(b));
+    if (c) atomicOr(&words[w0 + 2], bswap32(c));
+}
+
+// pass B: pack codewords MSB-first; uncodable members to `copied` in order
+__global__ void k_enc_pack(const uint32_t* __restrict__ arena, const uint64_t* __restrict__ off,
+                           const uint32_t* __restrict__ len, uint64_t lo, uint64_t hi,
+                           const uint64_t* __restrict__ code_bits, const uint8_t* __restrict__ code_len, int64_t top,
+                           const uint8_t* __restrict__ swap, const uint64_t* __restrict__ woff,
+                           const uint64_t* __restrict__ coff, uint32_t* __restrict__ words,
+                           uint32_t* __restrict__ copied) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t lt = lanemask_lt();
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t j = lo + w; j < hi; j += nw) {
+        const uint64_t k = j - lo;
+        const uint64_t b = off[j];
+        const uint32_t l = len[j];
+        uint32_t* out = words + woff[k];
+        uint32_t* cp = copied + coff[k];
+        const bool sw = swap[k];
+        uint64_t bitpos = 0;
+        uint32_t ncp = 0;
+        if (sw) {
+            if (lane == 0) put_code(out, 0, code_bits[top], code_len[top]);
+            bitpos = code_len[top];
+        }
+        for (uint32_t i0 = 0; i0 < l; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            uint32_t v = 0, L = 0;
+            bool unc = false;
+            if (i < l) {
+                v = arena[b + i];
+                L = code_len[v];
+                unc = L == 0;
+                if (sw && v == (uint32_t)top) L = 0;
+            }
+            uint32_t x = L;  // inclusive scan of code lengths
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            if (L) put_code(out, bitpos + x - L, code_bits[v], L);
+            const uint32_t um = __ballot_sync(FULL, unc);
+            if (unc) cp[ncp + __popc(um & lt)] = v;
+            ncp += __popc(um);
+            bitpos += __shfl_sync(FULL, x, 31);
+        }
+    }
+}
+
+// ---- bit reader over one set's stream -------------------------------------------
+struct BitReader {
+    const uint32_t* w;
+    uint64_t buf;
+    uint32_t nb;     // valid bits in buf (MSB-aligned)
+    uint32_t next;   // next word to load
+    __device__ void init(const uint32_t* words) {
+        w = words;
+        buf = 0;
+        nb = 0;
+        next = 0;
+        refill();
+        refill();
+    }
+    __device__ __forceinline__ void refill() {
+        if (nb <= 32) {
+            buf |= (uint64_t)bswap32(__ldg(w + next)) << (32 - nb);
+            nb += 32;
+            next++;
+        }
+    }
+    __device__ __forceinline__ uint32_t peek(uint32_t W) const { return (uint32_t)(buf >> (64 - W)); }
+    __device__ __forceinline__ void skip(uint32_t L) {
+        buf = L == 64 ? 0 : (buf << L);
+        nb -= L;
+        refill();
+    }
+};
+
+// decode one codeword; returns symbol, sets consumed bits; invalid -> false
+__device__ __forceinline__ bool decode_one(BitReader& br, const unsigned long long* __restrict__ lut, uint32_t root_bits,
+                                           uint32_t& sym, uint32_t& used) {
+    uint64_t toff = 0;
+    uint32_t W = root_bits;
+    used = 0;
+    for (;;) {
+        const unsigned long long e = __ldg(lut + toff + br.peek(W));
+        if (e >> 63) {
+            const uint32_t L = (uint32_t)(e >> 56) & 0x7f;
+            br.skip(L);
+            used += L;
+            sym = (uint32_t)e;
+            return true;
+        }
+        if (!((e >> 62) & 1)) return false;
+        br.skip(W);
+        used += W;
+        W = (uint32_t)(e >> 56) & 0x3f;
+        toff = e & 0xffffffffffffULL;
+    }
+}
+
+// select_huffman round: thread per live set
+__global__ void k_huff_round(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
+                             const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
+                             const uint32_t* __restrict__ copied, uint64_t count, const unsigned long long* __restrict__ lut,
+                             uint32_t root_bits, const uint32_t* __restrict__ cover_pick, uint8_t* __restrict__ deleted,
+                             unsigned int* __restrict__ hist, unsigned long long* __restrict__ maxdec) {
+    const uint32_t pick = *cover_pick;
+    if (pick == 0xffffffffu) return;
+    uint64_t local_max = 0;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += (uint64_t)gridDim.x * blockDim.x) {
+        if (deleted[j]) continue;
+        const uint32_t nbits = bits[j];
+        BitReader br;
+        br.init(words + woff[j]);
+        uint32_t pos = 0, nd = 0;
+        bool found = false;
+        while (pos < nbits) {
+            uint32_t sym, used;
+            if (!decode_one(br, lut, root_bits, sym, used)) break;  // cannot happen on our own streams
+            pos += used;
+            nd++;
+            if (sym == pick) {
+                found = true;
+                break;
+            }
+        }
+        if (!found)
+            for (uint64_t c = coff[j]; c < coff[j + 1]; ++c)
+                if (copied[c] == pick) {
+                    found = true;
+                    break;
+                }
+        local_max = nd > local_max ? nd : local_max;
+        if (found) {
+            deleted[j] = 1;
+            // the set leaves the live collection: subtract all its members
+            br.init(words + woff[j]);
+            pos = 0;
+            while (pos < nbits) {
+                uint32_t sym, used;
+                if (!decode_one(br, lut, root_bits, sym, used)) break;
+                pos += used;
+                atomicSub(&hist[sym], 1u);
+            }
+            for (uint64_t c = coff[j]; c < coff[j + 1]; ++c) atomicSub(&hist[copied[c]], 1u);
+        }
+    }
+    if (local_max) atomicMax(maxdec, (unsigned long long)local_max);
+}
+
+// decode_find on one set with every reference corruption check (huffman.cpp:129-158)
+// out[0]=status (1 found, 0 not, -2 invalid codeword, -3 mid-codeword), out[1]=n decoded
+__global__ void k_decode_find(const uint32_t* __restrict__ words, uint64_t woff, uint32_t nbits,
+                              const uint32_t* __restrict__ copied, uint64_t c0, uint64_t c1,
+                              const unsigned long long* __restrict__ lut, uint32_t root_bits, uint32_t top,
+                              uint32_t* __restrict__ decoded, long long* __restrict__ out) {
+    if (threadIdx.x || blockIdx.x) return;
+    BitReader br;
+    br.init(words + woff);
+    uint32_t pos = 0;
+    long long nd = 0;
+    while (pos < nbits) {
+        uint32_t sym, used;
+        if (!decode_one(br, lut, root_bits, sym, used)) {
+            out[0] = -2;
+            out[1] = nd;
+            return;
+        }
+        pos += used;
+        if (pos > nbits) {
+            out[0] = -3;
+            out[1] = nd;
+            return;
+        }
+        decoded[nd++] = sym;
+        if (sym == top) {
+            out[0] = 1;
+            out[1] = nd;
+            return;
+        }
+    }
+    out[1] = nd;
+    for (uint64_t c = c0; c < c1; ++c)
+        if (copied[c] == top) {
+            out[0] = 1;
+            return;
+        }
+    out[0] = 0;
+}
+
+__global__ void k_pick_from_key(const unsigned long long* __restrict__ keys, uint32_t r, uint8_t* __restrict__ is_seed,
+                                uint32_t* __restrict__ seeds, unsigned long long* __restrict__ marg,
+                                uint32_t* __restrict__ cover_pick, uint64_t n, uint32_t* __restrict__ padding) {
+    // padding persists: once a round had gain 0 the reference stops recounting (select.cpp:173-182)
+    const unsigned long long key = keys[r];
+    uint32_t pick = key ? 0xffffffffu - (uint32_t)(key & 0xffffffffu) : 0;
+    uint32_t gain = (uint32_t)(key >> 32);
+    if (*padding) gain = 0;
+    if (gain == 0) {
+        *padding = 1;
+        uint32_t p = 0;
+        while (p < n && is_seed[p]) ++p;
+        pick = p;
+        *cover_pick = 0xffffffffu;
+    } else {
+        *cover_pick = pick;
+    }
+    is_seed[pick] = 1;
+    seeds[r] = pick;
+    marg[r] = gain;
+}
+
+__global__ void k_add2(uint64_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t cnt, uint64_t da, uint64_t db) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
+        a[i] += da;
+        b[i] += db;
+    }
+}
+
+}  // namespace
+
+void store_set_codes(Store& S, Device& d, uint64_t n, const uint64_t* code_bits, const uint8_t* code_len,
+                     const std::vector<unsigned long long>& lut, uint32_t root_bits) {
+    cudaStream_t s = d.stream;
+    S.dev = &d;
+    S.n = n;
+    S.code_bits.exact(std::max<uint64_t>(n, 1));
+    S.code_len.exact(std::max<uint64_t>(n, 1));
+    CK(cudaMemcpyAsync(S.code_bits.p, code_bits, n * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(S.code_len.p, code_len, n, cudaMemcpyHostToDevice, s));
+    S.lut.exact(std::max<uint64_t>(lut.size(), 1));
+    if (!lut.empty()) CK(cudaMemcpyAsync(S.lut.p, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice, s));
+    S.lut_root_bits = root_bits;
+    S.lut_entries = lut.size();
+    S.woff.reserve(1, s);
+    S.coff.reserve(1, s);
+    uint64_t z = 0;
+    CK(cudaMemcpyAsync(S.woff.p, &z, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(S.coff.p, &z, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+// Encode sets [lo,hi) of the pool with the given top (or, when d_top_key != nullptr, the top
+// decoded on the device from an argmax key: no host round trip between blocks).
+// Returns the block's payload bytes (reference formula) through *payload_out when non-null.
+void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top, uint64_t* payload_out) {
+    Device& d = *S.dev;
+    cudaStream_t s = d.stream;
+    if (hi < lo || hi > P.count) fail(IMMX_ERANGE, "encode range out of bounds");
+    if (top >= (int64_t)S.n) fail(IMMX_ERANGE, "top out of range");
+    const uint64_t cnt = hi - lo;
+    if (cnt == 0) {
+        if (payload_out) *payload_out = 0;
+        return;
+    }
+    const uint64_t base = S.count;
+    S.woff.reserve(base + cnt + 1, s);
+    S.coff.reserve(base + cnt + 1, s);
+    S.bits.reserve(base + cnt, s);
+    DBuf<uint64_t> nwords, ncp;
+    DBuf<uint8_t> swap;
+    nwords.exact(cnt);
+    ncp.exact(cnt);
+    swap.exact(cnt);
+    unsigned long long* d_payload = d.scal.p + 16;
+    CK(cudaMemsetAsync(d_payload, 0, 8, s));
+    k_enc_size<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_len.p, top,
+                                                   S.bits.p + base, nwords.p, ncp.p, swap.p, d_payload);
+    CK_LAUNCH("k_enc_size");
+    d.kernel_launches++;
+    // exclusive scans, offset by the running totals: woff[base+1..] = total + inclusive
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, nwords.p, S.woff.p + base + 1, cnt, s);
+    size_t tb2 = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb2, ncp.p, S.coff.p + base + 1, cnt, s);
+    d.tmp.reserve(std::max(tb, tb2), s, false);
+    CK(cub::DeviceScan::InclusiveSum(d.tmp.p, tb, nwords.p, S.woff.p + base + 1, cnt, s));
+    CK(cub::DeviceScan::InclusiveSum(d.tmp.p, tb2, ncp.p, S.coff.p + base + 1, cnt, s));
+    uint64_t add[2];
+    CK(cudaMemcpyAsync(&add[0], S.woff.p + base + cnt, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&add[1], S.coff.p + base + cnt, 8, cudaMemcpyDeviceToHost, s));
+    unsigned long long payload = 0;
+    CK(cudaMemcpyAsync(&payload, d_payload, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    // shift the block's offsets by the store totals (they were scanned from 0)
+    const uint64_t w_total = S.total_words, c_total = S.total_copied;
+    if (w_total || c_total) {
+        k_add2<<<grid_for(cnt, d), 256, 0, s>>>(S.woff.p + base + 1, S.coff.p + base + 1, cnt, w_total, c_total);
+        CK_LAUNCH("k_add2");
+        d.kernel_launches++;
+    }
+    const uint64_t new_words = add[0], new_cp = add[1];
+    S.words.reserve(w_total + new_words + 4, s);
+    S.copied.reserve(c_total + new_cp + 1, s);
+    CK(cudaMemsetAsync(S.words.p + w_total, 0, (new_words + 4) * 4, s));
+    k_enc_pack<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_bits.p, S.code_len.p,
+                                                   top, swap.p, S.woff.p + base, S.coff.p + base, S.words.p,
+                                                   S.copied.p);
+    CK_LAUNCH("k_enc_pack");
+    d.kernel_launches++;
+    CK(cudaStreamSynchronize(s));
+    S.total_words = w_total + new_words;
+    S.total_copied = c_total + new_cp;
+    S.count = base + cnt;
+    S.payload_bytes += payload;
+    if (payload_out) *payload_out = payload;
+}
+
+void store_append_host(Store& S, const uint8_t* bytes, uint64_t n_bytes, uint64_t bit_length, const uint32_t* cp,
+                       uint64_t n_cp) {
+    Device& d = *S.dev;
+    cudaStream_t s = d.stream;
+    if (bit_length > n_bytes * 8) fail(IMMX_ERUNTIME, "encoded payload shorter than its bit length");
+    if (bit_length > 0xffffffffULL) fail(IMMX_EINVAL, "bit length too large");
+    const uint64_t base = S.count;
+    const uint64_t nw = (n_bytes + 3) / 4;
+    S.woff.reserve(base + 2, s);
+    S.coff.reserve(base + 2, s);
+    S.bits.reserve(base + 1, s);
+    S.words.reserve(S.total_words + nw + 4, s);
+    S.copied.reserve(S.total_copied + n_cp + 1, s);
+    std::vector<uint32_t> w(nw + 4, 0);
+    if (n_bytes) std::memcpy(w.data(), bytes, n_bytes);  // byte order in memory = stream order
+    CK(cudaMemcpyAsync(S.words.p + S.total_words, w.data(), (nw + 4) * 4, cudaMemcpyHostToDevice, s));
+    if (n_cp) CK(cudaMemcpyAsync(S.copied.p + S.total_copied, cp, n_cp * 4, cudaMemcpyHostToDevice, s));
+    const uint64_t wo = S.total_words + nw, co = S.total_copied + n_cp;
+    const uint32_t b32 = (uint32_t)bit_length;
+    CK(cudaMemcpyAsync(S.woff.p + base + 1, &wo, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(S.coff.p + base + 1, &co, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(S.bits.p + base, &b32, 4, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    S.total_words = wo;
+    S.total_copied = co;
+    S.count = base + 1;
+    S.payload_bytes += (bit_length + 7) / 8 + 4 * n_cp;
+}
+
+int store_decode_find(const Store& S, uint64_t j, uint32_t top, std::vector<uint32_t>& decoded) {
+    Device& d = *S.dev;
+    cudaStream_t s = d.stream;
+    if (j >= S.count) fail(IMMX_ERANGE, "set index out of range");
+    uint64_t wo[2], co[2];
+    uint32_t nbits = 0;
+    CK(cudaMemcpyAsync(wo, S.woff.p + j, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(co, S.coff.p + j, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&nbits, S.bits.p + j, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    DBuf<uint32_t> dec;
+    dec.exact((uint64_t)nbits + 1);
+    long long* out = reinterpret_cast<long long*>(d.scal.p + 24);
+    k_decode_find<<<1, 32, 0, s>>>(S.words.p, wo[0], nbits, S.copied.p, co[0], co[1], S.lut.p, S.lut_root_bits, top,
+                                   dec.p, out);
+    CK_LAUNCH("k_decode_find");
+    d.kernel_launches++;
+    long long h[2];
+    CK(cudaMemcpyAsync(h, out, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h[0] == -2) fail(IMMX_ERUNTIME, "corrupt payload: invalid codeword");
+    if (h[0] == -3) fail(IMMX_ERUNTIME, "corrupt payload: ends mid-codeword");
+    decoded.resize((size_t)h[1]);
+    if (h[1]) CK(cudaMemcpyAsync(decoded.data(), dec.p, (size_t)h[1] * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return (int)h[0];
+}
+
+// select.cpp:150-230 on the device.  d_hist: the encoding-time table (u32, consumed).
+void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& out, std::vector<uint64_t>* maxdec) {
+    Device& d = *S.dev;
+    cudaStream_t s = d.stream;
+    const uint64_t theta = S.count, n = S.n;
+    if (theta == 0) fail(IMMX_EINVAL, "selection requires at least one set");
+    if (k >= n) fail(IMMX_EINVAL, "selection requires k < n");
+    DBuf<uint8_t> deleted, is_seed;
+    deleted.exact(theta);
+    is_seed.exact(n);
+    CK(cudaMemsetAsync(deleted.p, 0, theta, s));
+    CK(cudaMemsetAsync(is_seed.p, 0, n, s));
+    DBuf<unsigned long long> keys, marg, mdec;
+    keys.exact(k);
+    marg.exact(k);
+    mdec.exact(k);
+    CK(cudaMemsetAsync(keys.p, 0, k * 8, s));
+    CK(cudaMemsetAsync(mdec.p, 0, k * 8, s));
+    DBuf<uint32_t> seeds, ctl;
+    seeds.exact(k);
+    ctl.exact(2);  // [0] cover pick, [1] padding flag
+    CK(cudaMemsetAsync(ctl.p, 0, 8, s));
+    const unsigned grid = grid_for(theta, d);
+    for (uint32_t r = 0; r < k; ++r) {
+        argmax_dev(d, d_hist, n, keys.p + r);
+        k_pick_from_key<<<1, 1, 0, s>>>(keys.p, r, is_seed.p, seeds.p, marg.p, ctl.p, n, ctl.p + 1);
+        k_huff_round<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, theta, S.lut.p,
+                                         S.lut_root_bits, ctl.p, deleted.p, d_hist, mdec.p + r);
+        CK_LAUNCH("select_huffman round");
+        d.kernel_launches += 2;
+    }
+    std::vector<uint32_t> hseeds(k);
+    std::vector<unsigned long long> hmarg(k), hmd(k);
+    CK(cudaMemcpyAsync(hseeds.data(), seeds.p, k * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hmarg.data(), marg.p, k * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hmd.data(), mdec.p, k * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    finish_select(hseeds, hmarg, theta, out);
+    if (maxdec) maxdec->assign(hmd.begin(), hmd.end());
+}
+
+// D2H of sets [lo,hi) in the reference's byte layout
+void store_read_host(const Store& S, uint64_t lo, uint64_t hi, uint64_t* byte_off, uint8_t* bytes, uint64_t* bit_length,
+                     uint64_t* cp_off, uint32_t* copied) {
+    Device& d = *S.dev;
+    cudaStream_t s = d.stream;
+    if (hi > S.count || lo > hi) fail(IMMX_ERANGE, "store range out of bounds");
+    const uint64_t cnt = hi - lo;
+    std::vector<uint64_t> wo(cnt + 1), co(cnt + 1);
+    std::vector<uint32_t> nb(cnt);
+    CK(cudaMemcpyAsync(wo.data(), S.woff.p + lo, (cnt + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(co.data(), S.coff.p + lo, (cnt + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (cnt) CK(cudaMemcpyAsync(nb.data(), S.bits.p + lo, cnt * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (bit_length)
+        for (uint64_t j = 0; j < cnt; ++j) bit_length[j] = nb[j];
+    if (byte_off || bytes) {
+        std::vector<uint64_t> bo(cnt + 1, 0);
+        for (uint64_t j = 0; j < cnt; ++j) bo[j + 1] = bo[j] + (nb[j] + 7) / 8;
+        if (byte_off) std::memcpy(byte_off, bo.data(), (cnt + 1) * 8);
+        if (bytes && cnt) {
+            std::vector<uint32_t> w(wo[cnt] - wo[0]);
+            if (!w.empty())
+                CK(cudaMemcpyAsync(w.data(), S.words.p + wo[0], w.size() * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            const uint8_t* wb = reinterpret_cast<const uint8_t*>(w.data());
+            for (uint64_t j = 0; j < cnt; ++j)
+                std::memcpy(bytes + bo[j], wb + (wo[j] - wo[0]) * 4, bo[j + 1] - bo[j]);
+        }
+    }
+    if (cp_off)
+        for (uint64_t j = 0; j <= cnt; ++j) cp_off[j] = co[j] - co[0];
+    if (copied && co[cnt] > co[0]) {
+        CK(cudaMemcpyAsync(copied, S.copied.p + co[0], (co[cnt] - co[0]) * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+}
+
+}  // namespace immx_dev

@@ -1,0 +1,226 @@
+// internal.hpp -- device-side objects behind the C-ABI handles (not exported).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "immx_b200.h"
+#include "common.cuh"
+
+namespace immx_dev {
+
+// Exceptions carry the C-ABI status they map to (reference error classes, SURVEY §5:
+// invalid_argument / runtime_error / out_of_range, plus CUDA failures).
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Error(code, m); }
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(IMMX_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ::immx_dev::cuda_check((x), #x)
+#define CK_LAUNCH(what) ::immx_dev::cuda_check(cudaGetLastError(), what)
+
+// A growable device buffer (never shrinks; contents preserved on growth).
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    uint64_t cap = 0;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    void reserve(uint64_t n, cudaStream_t s, bool keep = true) {
+        if (n <= cap) return;
+        uint64_t nc = cap ? cap : 1024;
+        while (nc < n) nc += nc / 2 + 1024;
+        T* q = nullptr;
+        CK(cudaMalloc(&q, nc * sizeof(T)));
+        if (keep && p && cap) CK(cudaMemcpyAsync(q, p, cap * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        if (p) {
+            CK(cudaStreamSynchronize(s));
+            cudaFree(p);
+        }
+        p = q;
+        cap = nc;
+    }
+    void exact(uint64_t n) {  // (re)allocate exactly n, contents undefined
+        if (n <= cap && n > 0) return;
+        release();
+        if (n) CK(cudaMalloc(&p, n * sizeof(T)));
+        cap = n;
+    }
+};
+
+struct Device {
+    int ordinal = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    uint64_t kernel_launches = 0;  // our kernels launched through this context
+    // small scratch
+    DBuf<unsigned long long> scal;  // general device scalars
+    DBuf<uint8_t> tmp;              // CUB temp storage
+    void* host_scal = nullptr;      // pinned host mirror of scal (64 x u64)
+};
+
+struct DevGraph {
+    Device* dev = nullptr;
+    uint64_t n = 0, m = 0;
+    DBuf<uint64_t> row;  // n+1   (reverse CSR offsets)
+    DBuf<uint32_t> col;  // m     (reverse CSR targets)
+    int pmode = kProbGlobal;
+    uint64_t gthr = 0;      // global threshold
+    DBuf<uint64_t> thr;     // per-row or per-edge thresholds
+    DBuf<double> lt_cum;    // LT: per-edge running weight sums in CSR order (row-local)
+    bool has_lt = false;
+    bool row_dups = false;  // some Gt row holds a repeated target
+    uint32_t max_deg = 0;
+};
+
+// Raw RRR pool: sets live in an arena (bump-allocated chunks); set j of the pool is
+// arena[off[j] .. off[j]+len[j]).  Sets are appended in batches of global indices.
+struct Pool {
+    Device* dev = nullptr;
+    DBuf<uint32_t> arena;
+    unsigned long long* cursor = nullptr;  // device bump pointer (in scal)
+    DBuf<uint64_t> off;
+    DBuf<uint32_t> len;
+    uint64_t count = 0;          // sets
+    uint64_t members = 0;        // sum of sizes
+    uint64_t edges = 0;          // sum of edges scanned while sampling
+    uint64_t arena_used = 0;     // arena cursor (host copy after each batch)
+    DBuf<unsigned long long> cur;  // the cursor itself
+};
+
+// Huffman-encoded store.  Set j: words[woff[j] ..] holds its MSB-first byte stream
+// (bytes in stream order in memory), bits[j] its bit length; copied[coff[j] .. coff[j+1]).
+struct Store {
+    Device* dev = nullptr;
+    uint64_t n = 0;
+    DBuf<uint64_t> code_bits;  // n
+    DBuf<uint8_t> code_len;    // n
+    DBuf<unsigned long long> lut;  // multi-level decode table
+    uint32_t lut_root_bits = 0;
+    uint64_t lut_entries = 0;
+    uint64_t count = 0;
+    DBuf<uint64_t> woff;   // count+1 word offsets
+    DBuf<uint32_t> bits;   // count
+    DBuf<uint64_t> coff;   // count+1
+    DBuf<uint32_t> words;
+    DBuf<uint32_t> copied;
+    uint64_t total_words = 0, total_copied = 0;
+    uint64_t payload_bytes = 0;  // reference formula: sum ceil(bits/8) + 4*copied
+};
+
+
+// ---------------------------------------------------------------- device operations ----
+struct SelectOut {
+    std::vector<uint32_t> seeds;
+    std::vector<uint64_t> marginal;
+    std::vector<double> coverage;
+    uint32_t padded = 0;
+};
+
+// device_graph.cu
+void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt,
+                  const double* prob, bool transposed);
+void graph_set_lt(DevGraph& G, const float* w);
+// sampler.cu
+void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first, uint64_t seed,
+                      const uint32_t* d_roots, const uint64_t* d_states, int model);
+// pool_select.cu
+void pool_hist_dev(const Pool& P, uint64_t lo, uint64_t hi, unsigned int* d_hist);
+void argmax_dev(Device& d, const unsigned int* d_hist, uint64_t n, unsigned long long* d_key);
+void u32_to_u64_dev(Device& d, const unsigned int* a, uint64_t n, uint64_t* b);
+void u64_to_u32_dev(Device& d, const uint64_t* a, uint64_t n, unsigned int* b);
+void finish_select(const std::vector<uint32_t>& seeds, const std::vector<unsigned long long>& marg, uint64_t theta,
+                   SelectOut& out);
+void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out);
+void pool_read_host(const Pool& P, uint64_t lo, uint64_t hi, uint64_t* offsets, uint32_t* members);
+void pool_upload_host(Pool& P, const uint64_t* offsets, const uint32_t* members, uint64_t count, uint64_t n_check);
+// huffman.cu
+void store_set_codes(Store& S, Device& d, uint64_t n, const uint64_t* code_bits, const uint8_t* code_len,
+                     const std::vector<unsigned long long>& lut, uint32_t root_bits);
+void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top, uint64_t* payload_out);
+void store_append_host(Store& S, const uint8_t* bytes, uint64_t n_bytes, uint64_t bit_length, const uint32_t* cp,
+                       uint64_t n_cp);
+int store_decode_find(const Store& S, uint64_t j, uint32_t top, std::vector<uint32_t>& decoded);
+void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& out, std::vector<uint64_t>* maxdec);
+void store_read_host(const Store& S, uint64_t lo, uint64_t hi, uint64_t* byte_off, uint8_t* bytes,
+                     uint64_t* bit_length, uint64_t* cp_off, uint32_t* copied);
+
+struct BitmapStore {
+    Device* dev = nullptr;
+    uint64_t n = 0;
+    struct Block {
+        uint64_t cols = 0, wpr = 0;
+        DBuf<uint32_t> words;
+    };
+    std::vector<Block*> blocks;
+    ~BitmapStore() {
+        for (auto* b : blocks) delete b;
+    }
+    uint64_t total_wpr() const {
+        uint64_t w = 0;
+        for (auto* b : blocks) w += b->wpr;
+        return w;
+    }
+    uint64_t total_cols() const {
+        uint64_t c = 0;
+        for (auto* b : blocks) c += b->cols;
+        return c;
+    }
+};
+
+// bitmap.cu
+void bitmap_encode_block(BitmapStore& B, const Pool& P, uint64_t lo, uint64_t hi);
+void bitmap_popcount(const BitmapStore& B, unsigned long long* d_hist64);
+void bitmap_row(const BitmapStore& B, uint32_t v, uint32_t* out);
+uint64_t bitmap_subtract_row(BitmapStore& B, uint32_t v, const uint32_t* snap);
+void select_bitmap_dev(BitmapStore& B, unsigned int* d_hist, uint32_t k, SelectOut& out);
+
+// ---------------------------------------------------------------- host helpers ----
+struct HostCodebook {
+    struct Node {
+        int32_t child[2] = {-1, -1};
+        uint32_t symbol = 0;
+    };
+    std::vector<uint64_t> bits;
+    std::vector<uint8_t> len;
+    std::vector<Node> nodes;  // nodes[0] = root
+    uint64_t coded = 0;
+};
+HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n);
+void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& lut, uint32_t& root_bits);
+
+}  // namespace immx_dev
+
+struct immx_device {
+    immx_dev::Device d;
+};
+struct immx_graph {
+    immx_dev::DevGraph g;
+};
+struct immx_pool {
+    immx_dev::Pool p;
+};
+struct immx_store {
+    immx_dev::Store s;
+};
+struct immx_bitmap {
+    immx_dev::BitmapStore b;
+};
+struct immx_hgraph {
+    uint64_t n = 0, m = 0;
+    std::vector<uint64_t> offsets;
+    std::vector<uint32_t> targets;
+    std::vector<double> probs;
+    std::vector<uint64_t> original_ids;
+};
+

@@ -1,0 +1,614 @@
+// sampler.cu -- RRR sampling on sm_100a (IC reverse BFS, LT reverse walk).
+//
+// Replaces the OpenMP loop of proj/src/sampler.cpp:85-104 (sample_block) and the body of
+// sample_rrr (sampler.cpp:14-45).  One warp owns one sample at a time (persistent grid,
+// dynamic work counter).  The sequential reference consumes one draw of the per-sample
+// stream (rng.hpp) per coin-tossing edge, in the order "adjacency rows of the members,
+// in member order".  The warp walks that flattened edge sequence in windows and assigns
+// draw numbers by ballot prefix:
+//   * an edge draws iff its target is unvisited *at that moment* and 0 < p < 1;
+//   * within one Gt row the targets are distinct (rows are deduplicated at upload, or the
+//     graph is flagged), so a group of U x 32 edges of one row is decided from the
+//     visited snapshot at the group start: U independent coins per lane (ILP);
+//   * a window that spans several rows may repeat a target: the window is committed up
+//     to the first lane whose target repeats an earlier candidate (match.any), and the
+//     rest is re-evaluated against the updated visited set.
+// Visited sets: a shared-memory bitmap over all n vertices when it fits, else a
+// shared-memory open-addressing hash with escalation (samples that overflow are
+// restarted from scratch -- the stream is a pure function of (seed, index) -- on a
+// bigger tier), and finally a per-warp global-memory bitmap.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "internal.hpp"
+
+namespace immx_dev {
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+struct GView {
+    uint64_t n;
+    const uint64_t* __restrict__ row;
+    const uint32_t* __restrict__ col;
+    const uint64_t* __restrict__ thr;  // per row or per edge, already shifted (T << 11)
+    const double* __restrict__ lt_cum;
+    uint64_t gthr;
+    int pmode;
+    int row_dups;
+};
+
+// shifted threshold: draw x succeeds iff x < (T << 11) (== (x >> 11) < T)
+__host__ __device__ __forceinline__ uint64_t shift_thr(uint64_t T) {
+    return (T == kThrNever || T == kThrAlways) ? T : (T << 11);
+}
+
+// The success test of one draw.  Only the high word decides unless it ties.
+__device__ __forceinline__ bool coin_success(uint64_t s0, uint64_t t, uint64_t tsh) {
+    uint64_t z = s0 + t * kGamma;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    const uint64_t y = z ^ (z >> 27);
+    const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
+    const uint32_t c2lo = 0x133111ebu, c2hi = 0x94d049bbu;
+    const uint32_t zhi = __umulhi(ylo, c2lo) + ylo * c2hi + yhi * c2lo;
+    const uint32_t xhi = zhi ^ (zhi >> 31);
+    const uint32_t thi = (uint32_t)(tsh >> 32);
+    if (xhi != thi) return xhi < thi;
+    const uint32_t zlo = ylo * c2lo;
+    const uint32_t xlo = zlo ^ ((zlo >> 31) | (zhi << 1));
+    return xlo < (uint32_t)tsh;
+}
+
+// ---------------------------------------------------------------- visited sets ----
+struct SmemBits {  // n bits in shared memory; never overflows
+    uint32_t* w;
+    uint32_t words;
+    __device__ bool has(uint32_t v) const { return (w[v >> 5] >> (v & 31)) & 1u; }
+    __device__ void add(uint32_t v) { atomicOr(&w[v >> 5], 1u << (v & 31)); }
+    __device__ void clear_all() {
+        for (uint32_t i = lane_id(); i < words; i += 32) w[i] = 0;
+    }
+    __device__ void clear_member(uint32_t v) { w[v >> 5] = 0; }
+    static constexpr bool kAlwaysFits = true;
+};
+
+struct GlobBits : SmemBits {};  // same layout, in global memory
+
+template <int LOGH>
+struct SmemHash {  // linear probing, load <= 1/2
+    uint32_t* s;
+    static constexpr uint32_t H = 1u << LOGH;
+    __device__ static uint32_t h(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - LOGH); }
+    __device__ bool has(uint32_t v) const {
+        uint32_t i = h(v);
+        for (;;) {
+            const uint32_t k = s[i];
+            if (k == v) return true;
+            if (k == kEmptyKey) return false;
+            i = (i + 1) & (H - 1);
+        }
+    }
+    __device__ void add(uint32_t v) {
+        uint32_t i = h(v);
+        for (;;) {
+            const uint32_t old = atomicCAS(&s[i], kEmptyKey, v);
+            if (old == kEmptyKey || old == v) return;
+            i = (i + 1) & (H - 1);
+        }
+    }
+    __device__ void clear_all() {
+        uint4 e = make_uint4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
+        for (uint32_t i = lane_id(); i < H / 4; i += 32) reinterpret_cast<uint4*>(s)[i] = e;
+    }
+    static constexpr bool kAlwaysFits = false;
+};
+
+// ------------------------------------------------------------------ one sample ----
+struct SampleResult {
+    uint32_t size;    // members written to q
+    uint64_t edges;   // edges of the members' rows (E_j)
+    bool overflow;
+};
+
+template <int U, class Vis>
+__device__ __forceinline__ SampleResult bfs_ic(const GView& g, Vis& vis, uint32_t* __restrict__ q, uint32_t qcap,
+                               uint32_t root, uint64_t s0, uint64_t t) {
+    const uint32_t lane = lane_id();
+    const uint32_t lt = lanemask_lt();
+    uint32_t qhead = 0, qlen = 1;
+    uint64_t edges = 0;
+    if (lane == 0) {
+        q[0] = root;
+        vis.add(root);
+    }
+    __syncwarp();
+    while (qhead < qlen) {
+        // ---- batch of up to 32 rows (members qhead..qhead+nb) ----
+        const uint32_t nb = min(32u, qlen - qhead);
+        uint64_t rs = 0, thr_r = g.gthr;
+        uint32_t deg = 0;
+        if (lane < nb) {
+            const uint32_t u = q[qhead + lane];
+            rs = g.row[u];
+            deg = (uint32_t)(g.row[u + 1] - rs);
+            if (g.pmode == kProbRow) thr_r = g.thr[u];
+        }
+        uint32_t cum = deg;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(FULL, cum, o);
+            if (lane >= (uint32_t)o) cum += x;
+        }
+        const uint32_t total = __shfl_sync(FULL, cum, 31);
+        edges += total;
+        qhead += nb;
+        uint32_t pos = 0;
+        while (pos < total) {
+            // row holding flattened position pos (warp-uniform)
+            const uint32_t r = __popc(__ballot_sync(FULL, cum <= pos));
+            const uint32_t r_end = __shfl_sync(FULL, cum, r);
+            if (!g.row_dups && (r_end - pos >= 32 || r_end == total)) {
+                // ---------- single-row run: groups of U x 32 edges, no repeats ----------
+                const uint32_t r_deg = __shfl_sync(FULL, deg, r);
+                const uint64_t r_rs = __shfl_sync(FULL, rs, r);
+                const uint64_t r_thr = __shfl_sync(FULL, thr_r, r);
+                uint64_t e0 = r_rs + (pos - (r_end - r_deg));
+                uint32_t left = r_end - pos;
+                pos = r_end;
+                while (left > 0) {
+                    const uint32_t here = min(left, (uint32_t)(U * 32));
+                    uint32_t v[U];
+                    uint64_t tt[U];
+                    bool cand[U];
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        const uint32_t k = i * 32 + lane;
+                        v[i] = k < here ? __ldg(g.col + e0 + k) : 0u;
+                        tt[i] = r_thr;
+                        if (g.pmode == kProbEdge && k < here) tt[i] = __ldg(g.thr + e0 + k);
+                    }
+                    uint32_t dmask[U];
+                    uint32_t draws_before = 0;
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        const uint32_t k = i * 32 + lane;
+                        cand[i] = k < here && tt[i] != kThrNever && !vis.has(v[i]);
+                        dmask[i] = __ballot_sync(FULL, cand[i] && tt[i] != kThrAlways);
+                    }
+                    bool succ[U];
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        const uint64_t my_t = t + draws_before + __popc(dmask[i] & lt);
+                        succ[i] = cand[i] && (tt[i] == kThrAlways || coin_success(s0, my_t, tt[i]));
+                        draws_before += __popc(dmask[i]);
+                    }
+                    t += draws_before;
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        const uint32_t sm = __ballot_sync(FULL, succ[i]);
+                        if (sm) {
+                            const uint32_t cnt = __popc(sm);
+                            if (qlen + cnt > qcap) return {qlen, edges, true};
+                            if (succ[i]) {
+                                q[qlen + __popc(sm & lt)] = v[i];
+                                vis.add(v[i]);
+                            }
+                            qlen += cnt;
+                        }
+                    }
+                    __syncwarp();
+                    e0 += here;
+                    left -= here;
+                }
+            } else {
+                // ---------- mixed window over several short rows ----------
+                const uint32_t gpos = pos + lane;
+                const bool valid = gpos < total;
+                // smallest row index rr with cum[rr] > gpos
+                uint32_t lo = 0, hi = 31;
+#pragma unroll
+                for (int s = 0; s < 5; ++s) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    const uint32_t c = __shfl_sync(FULL, cum, mid);
+                    if (c > gpos) hi = mid;
+                    else lo = mid + 1;
+                }
+                const uint32_t rr = valid ? lo : 31;
+                const uint32_t c_end = __shfl_sync(FULL, cum, rr);
+                const uint32_t c_deg = __shfl_sync(FULL, deg, rr);
+                const uint64_t c_rs = __shfl_sync(FULL, rs, rr);
+                uint64_t tsh = __shfl_sync(FULL, thr_r, rr);
+                uint32_t v = 0;
+                if (valid) {
+                    const uint64_t e = c_rs + (gpos - (c_end - c_deg));
+                    v = __ldg(g.col + e);
+                    if (g.pmode == kProbEdge) tsh = __ldg(g.thr + e);
+                }
+                const bool cand = valid && tsh != kThrNever && !vis.has(v);
+                // first lane whose candidate target repeats an earlier candidate
+                const unsigned long long key = cand ? (unsigned long long)v : (0x100000000ULL | lane);
+                const uint32_t peers = __match_any_sync(FULL, key);
+                const uint32_t dup = __ballot_sync(FULL, cand && (peers & lt) != 0);
+                const uint32_t cut = dup ? (uint32_t)(__ffs(dup) - 1) : 32u;
+                const bool in = lane < cut;
+                const uint32_t dm = __ballot_sync(FULL, in && cand && tsh != kThrAlways);
+                const uint64_t my_t = t + __popc(dm & lt);
+                const bool succ = in && cand && (tsh == kThrAlways || coin_success(s0, my_t, tsh));
+                t += __popc(dm);
+                const uint32_t sm = __ballot_sync(FULL, succ);
+                if (sm) {
+                    const uint32_t cnt = __popc(sm);
+                    if (qlen + cnt > qcap) return {qlen, edges, true};
+                    if (succ) {
+                        q[qlen + __popc(sm & lt)] = v;
+                        vis.add(v);
+                    }
+                    qlen += cnt;
+                }
+                __syncwarp();
+                pos += min(cut, total - pos);
+            }
+        }
+    }
+    return {qlen, edges, false};
+}
+
+// ------------------------------------------------------------------- LT walk ----
+// Extension (no reference implementation; oracle/immx_oracle.c oc_sample_lt is the
+// builder-defined contract): one draw r per step; the chosen in-edge is the first e of
+// the row with r < cum[e] (row-local running double sums, precomputed in CSR order);
+// stop on an empty row, r >= row sum, or an already visited target.
+template <class Vis>
+__device__ __forceinline__ SampleResult walk_lt(const GView& g, Vis& vis, uint32_t* __restrict__ q, uint32_t qcap,
+                                uint32_t root, uint64_t s0, uint64_t t) {
+    const uint32_t lane = lane_id();
+    uint32_t qlen = 1;
+    uint64_t edges = 0;
+    if (lane == 0) {
+        q[0] = root;
+        vis.add(root);
+    }
+    __syncwarp();
+    uint32_t cur = root;
+    for (;;) {
+        const uint64_t b = g.row[cur], e = g.row[cur + 1];
+        if (b == e) break;
+        const double r = (double)(draw(s0, t) >> 11) * 0x1.0p-53;
+        t++;
+        // first index with r < cum: warp-parallel search over 32-wide chunks
+        int64_t chosen = -1;
+        for (uint64_t base = b; base < e; base += 32) {
+            const uint64_t idx = base + lane;
+            const bool hit = idx < e && r < g.lt_cum[idx];
+            const uint32_t hm = __ballot_sync(FULL, hit);
+            if (hm) {
+                chosen = (int64_t)(base + __ffs(hm) - 1);
+                edges += (uint64_t)(chosen - b + 1);
+                break;
+            }
+        }
+        if (chosen < 0) {
+            edges += e - b;
+            break;
+        }
+        const uint32_t v = g.col[chosen];
+        if (vis.has(v)) break;
+        if (qlen + 1 > qcap) return {qlen, edges, true};
+        __syncwarp();
+        if (lane == 0) {
+            q[qlen] = v;
+            vis.add(v);
+        }
+        __syncwarp();
+        qlen++;
+        cur = v;
+    }
+    return {qlen, edges, false};
+}
+
+// ------------------------------------------------------------------ the kernel ----
+struct SampCtl {
+    unsigned int work;
+    unsigned int n_ovf;
+    unsigned int n_nospace;
+    unsigned int pad;
+    unsigned long long edges;
+    unsigned long long members;
+};
+
+struct SampJob {
+    uint64_t seed, first;            // seeded mode
+    const uint32_t* roots;           // rooted mode (nullptr -> seeded)
+    const uint64_t* states;
+    const uint32_t* list;            // sample indices to do (nullptr -> 0..count)
+    uint32_t count;
+    uint64_t pool_base;              // pool index of local sample 0
+    uint64_t* set_off;
+    uint32_t* set_len;
+    uint32_t* arena;
+    uint64_t arena_cap;
+    unsigned long long* cursor;
+    uint32_t* ovf_list;
+    uint32_t* nospace_list;
+    SampCtl* ctl;
+    uint32_t* qscratch;              // per-warp queue scratch (qcap entries each)
+    uint32_t* gbits;                 // per-warp global bitmap (GlobBits tier)
+    uint32_t qcap;
+    int model;
+};
+
+enum VisKind { kVisSmemBits = 0, kVisHash11 = 1, kVisHash13 = 2, kVisHash15 = 3, kVisGlobBits = 4 };
+
+template <int KIND>
+struct VisOf;
+template <>
+struct VisOf<kVisSmemBits> { using T = SmemBits; };
+template <>
+struct VisOf<kVisHash11> { using T = SmemHash<11>; };
+template <>
+struct VisOf<kVisHash13> { using T = SmemHash<13>; };
+template <>
+struct VisOf<kVisHash15> { using T = SmemHash<15>; };
+template <>
+struct VisOf<kVisGlobBits> { using T = GlobBits; };
+
+template <int KIND>
+__device__ __forceinline__ typename VisOf<KIND>::T make_vis(uint32_t* smem_warp, uint32_t* gbits_warp,
+                                                            uint64_t n) {
+    typename VisOf<KIND>::T vis;
+    if constexpr (KIND == kVisSmemBits) {
+        vis.w = smem_warp;
+        vis.words = (uint32_t)((n + 31) / 32);
+    } else if constexpr (KIND == kVisGlobBits) {
+        vis.w = gbits_warp;
+        vis.words = (uint32_t)((n + 31) / 32);
+    } else {
+        vis.s = smem_warp;
+    }
+    return vis;
+}
+
+template <int KIND, int U>
+__global__ void __launch_bounds__(256) rrr_kernel(GView g, SampJob job, uint32_t smem_words_per_warp) {
+    extern __shared__ uint32_t smem[];
+    const uint32_t warp_in_block = threadIdx.x >> 5;
+    const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + warp_in_block;
+    const uint32_t lane = lane_id();
+    uint32_t* my_smem = smem + (size_t)warp_in_block * smem_words_per_warp;
+    uint32_t* my_gbits = job.gbits ? job.gbits + (size_t)gwarp * ((g.n + 31) / 32) : nullptr;
+    uint32_t* q = job.qscratch + (size_t)gwarp * job.qcap;
+    auto vis = make_vis<KIND>(my_smem, my_gbits, g.n);
+    if constexpr (KIND != kVisGlobBits) vis.clear_all();  // the host zeroes global bitmaps
+    __syncwarp();
+    for (;;) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(&job.ctl->work, 1u);
+        idx = __shfl_sync(FULL, idx, 0);
+        if (idx >= job.count) break;
+        const uint32_t j = job.list ? job.list[idx] : idx;
+        uint64_t s0;
+        uint32_t root;
+        uint64_t t;
+        if (job.roots) {
+            s0 = job.states[j];
+            root = job.roots[j];
+            t = 1;
+        } else {
+            s0 = stream_state(job.seed, job.first + j);
+            root = (uint32_t)below(draw(s0, 1), g.n);
+            t = 2;
+        }
+        SampleResult res = job.model == IMMX_MODEL_LT ? walk_lt(g, vis, q, job.qcap, root, s0, t)
+                                                       : bfs_ic<U>(g, vis, q, job.qcap, root, s0, t);
+        __syncwarp();
+        if (!res.overflow) {
+            // reserve exactly |R| arena slots and copy the set out
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(job.cursor, (unsigned long long)res.size);
+            base = __shfl_sync(FULL, base, 0);
+            if (base + res.size > job.arena_cap) {
+                if (lane == 0) job.nospace_list[atomicAdd(&job.ctl->n_nospace, 1u)] = j;
+            } else {
+                for (uint32_t i = lane; i < res.size; i += 32) job.arena[base + i] = q[i];
+                if (lane == 0) {
+                    job.set_off[job.pool_base + j] = base;
+                    job.set_len[job.pool_base + j] = res.size;
+                    atomicAdd(&job.ctl->edges, (unsigned long long)res.edges);
+                    atomicAdd(&job.ctl->members, (unsigned long long)res.size);
+                }
+            }
+        } else if (lane == 0) {
+            job.ovf_list[atomicAdd(&job.ctl->n_ovf, 1u)] = j;
+        }
+        // reset the visited set for the next sample
+        if constexpr (KIND == kVisGlobBits) {
+            for (uint32_t i = lane; i < res.size; i += 32) vis.clear_member(q[i]);
+        } else if constexpr (KIND == kVisSmemBits) {
+            if (res.size > vis.words / 4) {
+                __syncwarp();
+                vis.clear_all();
+            } else {
+                for (uint32_t i = lane; i < res.size; i += 32) vis.clear_member(q[i]);
+            }
+        } else {
+            vis.clear_all();
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------- host side ----
+namespace {
+
+struct Tier {
+    int kind;
+    uint32_t smem_words_per_warp;  // 0 for global tiers
+    uint32_t warps_per_block;
+    uint32_t qcap;
+};
+
+template <int KIND>
+void launch_tier(Device& d, const GView& gv, SampJob job, const Tier& tier, uint32_t nitems) {
+    const uint32_t wpb = tier.warps_per_block;
+    const size_t smem = (size_t)tier.smem_words_per_warp * 4 * wpb;
+    auto kern = rrr_kernel<KIND, 4>;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)(wpb * 32), smem));
+    if (per_sm < 1) fail(IMMX_ECUDA, "sampler tier does not fit on an SM");
+    uint32_t blocks = (uint32_t)per_sm * (uint32_t)d.num_sms;
+    const uint32_t need_warps = (nitems + 0) ;
+    blocks = std::min<uint32_t>(blocks, std::max<uint32_t>(1, (need_warps + wpb - 1) / wpb));
+    job.qcap = tier.qcap;
+    kern<<<blocks, wpb * 32, smem, d.stream>>>(gv, job, tier.smem_words_per_warp);
+    CK_LAUNCH("rrr_kernel");
+    d.kernel_launches++;
+}
+
+uint32_t grid_warps(Device& d, const Tier& t) {
+    // an upper bound of the warps launch_tier may start (for scratch sizing)
+    const size_t smem = (size_t)t.smem_words_per_warp * 4 * t.warps_per_block;
+    const uint32_t per_sm_smem = smem ? (uint32_t)std::max<size_t>(1, (227 * 1024) / smem) : 32;
+    const uint32_t per_sm = std::min<uint32_t>(per_sm_smem, 64 / t.warps_per_block);
+    return per_sm * t.warps_per_block * (uint32_t)d.num_sms;
+}
+
+}  // namespace
+
+GView make_view(const DevGraph& g) {
+    GView v;
+    v.n = g.n;
+    v.row = g.row.p;
+    v.col = g.col.p;
+    v.thr = g.thr.p;
+    v.gthr = g.gthr;
+    v.pmode = g.pmode;
+    v.row_dups = g.row_dups ? 1 : 0;
+    v.lt_cum = g.lt_cum.p;
+    return v;
+}
+
+// Append `count` samples to the pool.  roots/states (device pointers) select rooted mode.
+void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first, uint64_t seed,
+                      const uint32_t* d_roots, const uint64_t* d_states, int model) {
+    Device& d = *P.dev;
+    cudaStream_t s = d.stream;
+    if (count == 0) return;
+    if (count > 0xffffffffULL) fail(IMMX_EINVAL, "sample batch larger than 2^32");
+    if (G.n == 0) fail(IMMX_EINVAL, "graph has no vertices");
+    if (model == IMMX_MODEL_LT && !G.has_lt) fail(IMMX_EINVAL, "LT model requires per-edge LT weights");
+    const uint64_t base = P.count;
+    P.off.reserve(base + count, s);
+    P.len.reserve(base + count, s);
+    // arena: grow to an estimate (mean size so far, else 8 per sample)
+    const double mean = P.count ? (double)P.members / (double)P.count : 8.0;
+    const uint64_t want = P.arena_used + (uint64_t)(mean * 1.25 * (double)count) + 4096;
+    P.arena.reserve(want, s);
+    P.cur.reserve(1, s);
+    CK(cudaMemcpyAsync(P.cur.p, &P.arena_used, 8, cudaMemcpyHostToDevice, s));
+
+    // tiers
+    std::vector<Tier> tiers;
+    const uint64_t nwords = (G.n + 31) / 32;
+    if (nwords * 4 <= 40 * 1024) {
+        const uint32_t bytes = (uint32_t)(nwords * 4);
+        uint32_t wpb = 8;
+        while (wpb > 1 && (uint64_t)bytes * wpb > 100 * 1024) wpb /= 2;
+        tiers.push_back({kVisSmemBits, (uint32_t)nwords, wpb, (uint32_t)std::min<uint64_t>(G.n, 0xffffffffu)});
+    } else {
+        tiers.push_back({kVisHash11, 1u << 11, 8, 1u << 10});
+        tiers.push_back({kVisHash13, 1u << 13, 2, 1u << 12});
+        tiers.push_back({kVisHash15, 1u << 15, 1, 1u << 14});
+        tiers.push_back({kVisGlobBits, 0, 4, (uint32_t)std::min<uint64_t>(G.n, 0xffffffffu)});
+    }
+
+    DBuf<uint32_t> lists[2];
+    DBuf<uint32_t> nospace;
+    DBuf<uint32_t> qscratch;
+    DBuf<uint32_t> gbits;
+    DBuf<SampCtl> ctl;
+    ctl.exact(1);
+    SampCtl* hctl = static_cast<SampCtl*>(d.host_scal);
+    lists[0].exact(count);
+    lists[1].exact(count);
+    nospace.exact(count);
+
+    GView gv = make_view(G);
+    SampJob job{};
+    job.seed = seed;
+    job.first = first;
+    job.roots = d_roots;
+    job.states = d_states;
+    job.pool_base = base;
+    job.set_off = P.off.p;
+    job.set_len = P.len.p;
+    job.cursor = P.cur.p;
+    job.ctl = ctl.p;
+    job.model = model;
+
+    const uint32_t* cur_list = nullptr;  // identity
+    uint32_t nitems = (uint32_t)count;
+    int in_buf = 0;
+    unsigned long long edges = 0, members = 0;
+    for (size_t ti = 0; ti < tiers.size() && nitems > 0;) {
+        const Tier& tier = tiers[ti];
+        const uint32_t warps = grid_warps(d, tier);
+        qscratch.reserve((uint64_t)warps * tier.qcap, s, false);
+        if (tier.kind == kVisGlobBits) {
+            gbits.reserve((uint64_t)warps * nwords, s, false);
+            CK(cudaMemsetAsync(gbits.p, 0, (size_t)warps * nwords * 4, s));
+        }
+        CK(cudaMemsetAsync(ctl.p, 0, sizeof(SampCtl), s));
+        job.list = cur_list;
+        job.count = nitems;
+        job.arena = P.arena.p;
+        job.arena_cap = P.arena.cap;
+        job.ovf_list = lists[in_buf ^ 1].p;
+        job.nospace_list = nospace.p;
+        job.qscratch = qscratch.p;
+        job.gbits = gbits.p;
+        switch (tier.kind) {
+            case kVisSmemBits: launch_tier<kVisSmemBits>(d, gv, job, tier, nitems); break;
+            case kVisHash11: launch_tier<kVisHash11>(d, gv, job, tier, nitems); break;
+            case kVisHash13: launch_tier<kVisHash13>(d, gv, job, tier, nitems); break;
+            case kVisHash15: launch_tier<kVisHash15>(d, gv, job, tier, nitems); break;
+            default: launch_tier<kVisGlobBits>(d, gv, job, tier, nitems); break;
+        }
+        CK(cudaMemcpyAsync(hctl, ctl.p, sizeof(SampCtl), cudaMemcpyDeviceToHost, s));
+        unsigned long long cursor = 0;
+        CK(cudaMemcpyAsync(&cursor, P.cur.p, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        edges += hctl->edges;
+        members += hctl->members;
+        const uint32_t n_ovf = hctl->n_ovf, n_nospace = hctl->n_nospace;
+        if (n_nospace) {
+            // grow the arena past everything reserved so far and redo those samples here
+            const uint64_t grow = std::max<uint64_t>((uint64_t)cursor + (uint64_t)(mean * 2.0 * n_nospace) + 65536,
+                                                     P.arena.cap + P.arena.cap / 2);
+            P.arena.reserve(grow, s);
+            // merge: the nospace samples go first through the same tier again
+            CK(cudaMemcpyAsync(lists[in_buf ^ 1].p + n_ovf, nospace.p, (size_t)n_nospace * 4,
+                               cudaMemcpyDeviceToDevice, s));
+            // re-run the same tier over ovf+nospace only if the tier can hold them; simplest:
+            // overflowed ones will simply overflow again (cheap: they are rare)
+            cur_list = lists[in_buf ^ 1].p;
+            in_buf ^= 1;
+            nitems = n_ovf + n_nospace;
+            continue;  // same tier
+        }
+        cur_list = lists[in_buf ^ 1].p;
+        in_buf ^= 1;
+        nitems = n_ovf;
+        ++ti;
+    }
+    if (nitems) fail(IMMX_ERUNTIME, "sampler: samples left after the last tier");
+    unsigned long long cursor = 0;
+    CK(cudaMemcpyAsync(&cursor, P.cur.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    P.arena_used = cursor;
+    P.count = base + count;
+    P.members += members;
+    P.edges += edges;
+}
+
+}  // namespace immx_dev

@@ -1,0 +1,282 @@
+"""Pin the C restatement oracle (oracle/immx_oracle.c) to the reference's own known-answer
+tests.  Each case cites the reference test it restates (proj/tests/...)."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import make_csr, random_graph, random_sets, sets_csr
+
+
+def test_theta_kat(orc):
+    # test_sampler.cpp:77, test_smoke.py:32
+    assert orc.theta_bound(100, 1, 0.5, 1) == 229
+    a = orc.theta_bound_real(1000, 5, 0.3, 2)
+    assert orc.theta_bound_real(1000, 5, 0.3, 3) == 2 * a
+
+
+def _theta_oracle(n, k, eps, i):  # test_util.hpp:134-142 (sum of logs)
+    lb = sum(math.log(n - k + j) - math.log(j) for j in range(1, k + 1))
+    nd = float(n)
+    bracket = lb * math.log(nd) + math.log(math.log2(nd))
+    return (2.0 + 2.0 * math.sqrt(2.0) / 3.0 * eps) * bracket * 2.0 ** i / (2.0 * eps * eps)
+
+
+@pytest.mark.parametrize("n", [10, 100, 5000, 1000000])
+@pytest.mark.parametrize("k", [1, 5, 9])
+def test_theta_eq1(orc, n, k):
+    # test_sampler.cpp:76-90
+    for eps in (0.1, 0.5):
+        for i in (1, 3):
+            assert orc.theta_bound_real(n, k, eps, i) == pytest.approx(_theta_oracle(n, k, eps, i), rel=1e-9)
+
+
+def test_chain_p1(orc):
+    # test_sampler.cpp:14-20: transpose holds c->b->a, rooting at c reaches all
+    gt = make_csr(3, [(2, 1, 1.0), (1, 0, 1.0)])
+    assert orc.sample_rrr(gt, 2, 123) == [2, 1, 0]
+
+
+def test_p0_singletons(orc):
+    # test_sampler.cpp:22-29, :139-144
+    edges = [(u, v, 0.0) for u in range(5) for v in range(5) if u != v]
+    gt = orc.transpose(make_csr(5, edges))
+    for v in range(5):
+        assert orc.sample_rrr(gt, v, 9) == [v]
+    off, mem, _ = orc.sample_block(gt, 50, 0, 5)
+    assert np.all(np.diff(off.astype(np.int64)) == 1)
+
+
+def test_star_mean(orc):
+    # test_sampler.cpp:31-41: mean size 1 + 2*0.5 over stream_for(77, t)
+    gt = make_csr(3, [(0, 1, 0.5), (0, 2, 0.5)])
+    # rooted at 0 with Rng = stream_for(77, t), coins from the first draw
+    tot = 0
+    L = orc.L
+    out = np.zeros(4, np.uint32)
+    for t in range(10000):
+        st = orc.stream_state(77, t)
+        r = L.oc_sample_rrr_seed(3, gt.off, gt.tgt, gt.prob, 0, st, out, 4)
+        tot += r
+    assert tot / 10000 == pytest.approx(2.0, rel=0.05)
+
+
+def test_p1_equals_bfs(orc):
+    # test_sampler.cpp:59-74
+    rng = np.random.default_rng(21)
+    for _ in range(30):
+        g = random_graph(rng, 25, 80)
+        g = orc.assign_weights(g, "uniform", 1.0)
+        gt = orc.transpose(g)
+        for root in range(0, 25, 7):
+            got = sorted(orc.sample_rrr(gt, root, root))
+            seen, q = {root}, [root]
+            while q:
+                u = q.pop()
+                for e in range(int(gt.off[u]), int(gt.off[u + 1])):
+                    v = int(gt.tgt[e])
+                    if v not in seen:
+                        seen.add(v)
+                        q.append(v)
+            assert got == sorted(seen)
+
+
+def test_estimate_theta_k4_and_cap(orc):
+    # test_sampler.cpp:146-164
+    edges = [(u, v, 1.0) for u in range(4) for v in range(4) if u != v]
+    gt = orc.transpose(make_csr(4, edges))
+    p = orc.estimate_theta(gt, 1, 0.5, 42)
+    assert p["exit_iteration"] == 1 and p["covered_fraction"] == 1.0 and p["theta"] >= p["estimation_samples"]
+    gt2 = orc.transpose(make_csr(2, [(0, 1, 0.0)]))
+    p2 = orc.estimate_theta(gt2, 1, 0.5, 3)
+    assert p2["exit_iteration"] == 0 and p2["theta"] == p2["estimation_samples"]
+    F = p2["covered_fraction"]  # doctest Approx(0.5).epsilon(0.15): |F-0.5| < 0.15*(1+max)
+    assert abs(F - 0.5) < 0.15 * (1 + max(F, 0.5))
+
+
+def test_characterize(orc):
+    # test_characterize.cpp:40-43, test_smoke.py:36-41
+    assert orc.skewness([1, 1, 1, 10]) == pytest.approx(1.1547, abs=1e-4)
+    assert orc.skewness([2, 4, 6]) == 0.0
+    assert orc.density([5, 5], 10) == 0.5
+    assert orc.choose_encoding(11.46, 0.00261) == "huffman"
+    assert orc.choose_encoding(-1.43, 0.6601) == "bitmap"
+    assert orc.choose_encoding(-0.5, 0.01) == "raw"
+    assert orc.choose_encoding(-0.1, 1.0 / 32.0) == "raw"
+    assert orc.choose_encoding(0.0, 0.001) == "huffman"
+
+
+def test_huffman_lengths(orc):
+    # test_huffman.cpp:72-97
+    cb = orc.codebook([5, 2, 1])
+    assert cb.lens.tolist() == [1, 2, 2] and cb.coded_vertices == 3
+    assert sum(2 ** (64 - int(l)) for l in cb.lens) == 2 ** 64
+    assert orc.codebook([1, 1, 1, 1]).lens.tolist() == [2, 2, 2, 2]
+    one = orc.codebook([0, 7, 0])
+    assert one.lens[1] == 1 and one.coded_vertices == 1
+    data, bl, cp = one.encode([1])
+    assert bl == 1
+    assert one.decode_find(data, bl, cp, 99) == (False, [1])
+
+
+def test_huffman_monotone(orc):
+    # test_huffman.cpp:99-118
+    rng = np.random.default_rng(12)
+    for _ in range(50):
+        f = rng.integers(0, 501, 40)
+        f[0] = 1
+        cb = orc.codebook(f)
+        for a in range(40):
+            for b in range(40):
+                if f[a] and f[b] and f[a] > f[b]:
+                    assert cb.lens[a] <= cb.lens[b]
+        if cb.coded_vertices >= 2:
+            assert sum(2 ** (64 - int(l)) for l in cb.lens if l) == 2 ** 64
+
+
+def test_bitstream_kat(orc):
+    # test_huffman.cpp:124-136 with the a=0, b=10, c=11 codebook: freq {2,1,1} gives exactly
+    # those lengths; the oracle must produce MSB-first bytes, top first.
+    cb = orc.codebook([2, 1, 1])
+    # tree: pop (1,1) (1,2) -> inner(2,min 1); pop (2,0) leaf0? heap has (2,0,leaf0),(2,1,inner)
+    # -> leaf0 branch 0 => a=0, inner branch 1: b=10, c=11
+    assert [cb.code(v) for v in range(3)] == ["0", "10", "11"]
+    data, bl, cp = cb.encode([1, 0, 2], top=0)
+    assert bl == 5 and data == bytes([0b01011000]) and cp == []
+    assert cb.decode_find(data, bl, cp, 0) == (True, [0])
+    data2, bl2, cp2 = cb.encode([1, 2], top=0)
+    assert cb.decode_find(data2, bl2, cp2, 0) == (False, [1, 2])
+
+
+def test_copy_buffer_and_corruption(orc):
+    # test_huffman.cpp:146-168
+    cb = orc.codebook([5, 2, 1, 0])
+    data, bl, cp = cb.encode([3, 0, 1])
+    assert cp == [3]
+    found, dec = cb.decode_find(data, bl, cp, 3)
+    assert found and len(dec) == 2
+    cb2 = orc.codebook([5, 2, 1])
+    data, bl, cp = cb2.encode([1, 2])
+    with pytest.raises(RuntimeError):
+        cb2.decode_find(data, 3, cp, 0)
+    with pytest.raises(RuntimeError):
+        cb2.decode_find(data, 64, cp, 0)
+
+
+def test_huffman_round_trip(orc):
+    # test_huffman.cpp:170-199
+    rng = np.random.default_rng(77)
+    for _ in range(60):
+        n = 60
+        cb = orc.codebook_from_sets(random_sets(rng, n, 40, 12), n)
+        for members in random_sets(rng, n, 20, 12):
+            top = int(rng.integers(0, n))
+            data, bl, cp = cb.encode(members, top)
+            found, dec = cb.decode_find(data, bl, cp, n + 1)
+            assert not found and sorted(dec + cp) == sorted(members)
+            assert cb.decode_find(data, bl, cp, top)[0] == (top in members)
+
+
+def test_select_worked_examples(orc):
+    # test_select.cpp:69-98
+    off, mem = sets_csr([[1, 2], [1, 3], [4]])
+    s = orc.select_raw(off, mem, 5, 2)
+    assert s["seeds"] == [1, 4] and s["coverage"][0] == pytest.approx(2 / 3) and s["coverage"][1] == 1.0
+    off, mem = sets_csr([[2], [1]])
+    assert orc.select_raw(off, mem, 3, 1)["seeds"] == [1]
+    off, mem = sets_csr([[1], [1]])
+    s = orc.select_raw(off, mem, 5, 3)
+    assert s["seeds"] == [1, 0, 2] and s["padded"] == 2 and s["marginal"] == [2, 0, 0]
+
+
+def _brute(sets, n, k):  # test_util.hpp:93-130
+    dead = [False] * len(sets)
+    chosen = [False] * n
+    seeds, marg = [], []
+    for _ in range(k):
+        cnt = [0] * n
+        for j, s in enumerate(sets):
+            if not dead[j]:
+                for v in s:
+                    cnt[v] += 1
+        best = 0
+        for v in range(1, n):
+            if cnt[v] > cnt[best]:
+                best = v
+        if cnt[best] == 0:
+            best = chosen.index(False)
+        gain = 0
+        for j, s in enumerate(sets):
+            if not dead[j] and best in s:
+                dead[j] = True
+                gain += 1
+        chosen[best] = True
+        seeds.append(best)
+        marg.append(gain)
+    return seeds, marg
+
+
+def test_select_brute_force(orc):
+    # test_select.cpp:100-111
+    rng = np.random.default_rng(41)
+    for trial in range(60):
+        n = 5 + trial % 26
+        sets = random_sets(rng, n, 3 + trial % 48, 6)
+        k = 1 + trial % min(10, n - 1)
+        off, mem = sets_csr(sets)
+        got = orc.select_raw(off, mem, n, k)
+        assert (got["seeds"], got["marginal"]) == _brute(sets, n, k)
+
+
+def test_huffman_and_bitmap_equal_raw(orc):
+    # test_select.cpp:113-157
+    rng = np.random.default_rng(17)
+    for trial in range(40):
+        n = 10 + trial % 40
+        sets = random_sets(rng, n, 5 + trial % 60, 8)
+        k = 1 + trial % 6
+        off, mem = sets_csr(sets)
+        raw = orc.select_raw(off, mem, n, k)
+        hist = np.bincount(mem, minlength=n).astype(np.uint64)
+        cb = orc.codebook(hist)
+        store = cb.store(off, mem, orc.table_argmax(hist))
+        huf = store.select(hist, k)
+        bm = orc.select_bitmap_sets(off, mem, n, k, 1 + trial % 3)
+        for x in (huf, bm):
+            assert (x["seeds"], x["marginal"], x["coverage"], x["padded"]) == (
+                raw["seeds"], raw["marginal"], raw["coverage"], raw["padded"])
+
+
+def test_uncoded_top_deleted(orc):
+    # test_select.cpp:134-143
+    warm = [[1, 2], [3]]
+    sets = [[0, 1], [0, 2], [0, 3], [3]]
+    n = 5
+    cb = orc.codebook_from_sets(warm, n)
+    off, mem = sets_csr(sets)
+    hist = np.bincount(mem, minlength=n).astype(np.uint64)
+    s = cb.store(off, mem, orc.table_argmax(hist)).select(hist, 2)
+    assert s["seeds"] == orc.select_raw(off, mem, n, 2)["seeds"] and s["seeds"][0] == 0 and s["marginal"][0] == 3
+
+
+def test_bitmap_worked_matrix(orc):
+    # test_bitmap.cpp:47-93, test_select.cpp:159-170
+    sets = [[0, 2], [0, 1, 3], [1, 2, 4], [3, 4], [0, 2, 4], [0, 1, 3]]
+    off, mem = sets_csr(sets)
+    w = orc.bitmap_block(off, mem, 0, 6, 5)
+    rows = [[(int(w[v, 0]) >> c) & 1 for c in range(6)] for v in range(5)]
+    assert rows == [[1, 1, 0, 0, 1, 1], [0, 1, 1, 0, 0, 1], [1, 0, 1, 0, 1, 0], [0, 1, 0, 1, 0, 1], [0, 0, 1, 1, 1, 0]]
+    assert orc.select_bitmap_sets(off, mem, 5, 1)["seeds"] == [0]
+    assert orc.select_bitmap_sets(off, mem, 5, 2)["seeds"] == [0, 4]
+    off, mem = sets_csr([[1]])
+    b = orc.select_bitmap_sets(off, mem, 4, 3)
+    assert b["padded"] == 2 and b["seeds"] == orc.select_raw(off, mem, 4, 3)["seeds"]
+
+
+def test_pipeline_modes_agree(orc):
+    # test_pipeline.cpp:52-67, test_smoke.py:74-92
+    rng = np.random.default_rng(12)
+    for trial in range(3):
+        g = orc.assign_weights(random_graph(rng, 40 + 20 * trial, 300 + 100 * trial), "wc")
+        res = [orc.run(g, 5, 0.5, 4, m, 100 + trial)["seeds"] for m in ("raw", "huffman", "bitmap")]
+        assert res[0] == res[1] == res[2]
