@@ -112,6 +112,21 @@ IMMX_API void immx_device_destroy(immx_device* d);
 IMMX_API void* immx_device_stream(immx_device* d);            /* the cudaStream_t all calls use */
 IMMX_API int immx_device_synchronize(immx_device* d);
 IMMX_API uint64_t immx_device_kernel_launches(const immx_device* d); /* our kernels launched so far */
+/* Per-kernel-class profile: when enabled, launches of the classes below are bracketed by
+ * CUDA events on the device stream; bytes are ALGORITHMIC bytes:
+ *   SAMPLE : 12*|R_j| + 4*E_j + 8 per committed sample (+4*E_j per-edge probs / LT weights)
+ *   ENCODE : 4*|R_j| read + payload written, per encoded set
+ *   HSELECT: payload of every live set scanned + decremented members, per round
+ *   RSELECT: 4*|R_j| of every covered set + 4n argmax, per round */
+#define IMMX_KSTAT_SAMPLE 0
+#define IMMX_KSTAT_ENCODE 1
+#define IMMX_KSTAT_HSELECT 2
+#define IMMX_KSTAT_RSELECT 3
+#define IMMX_KSTAT_ARGMAX 4
+IMMX_API int immx_device_profile(immx_device* d, int enable);
+IMMX_API int immx_device_kernel_stats(const immx_device* d, int kind, uint64_t* launches, double* ms,
+                                      uint64_t* bytes);
+IMMX_API int immx_device_reset_stats(immx_device* d);
 
 /* ----------------------------------------------------------------- device graph --- */
 /* Upload a graph: transposed != 0 -> the arrays already are Gt (sample_block/estimate_theta

@@ -58,6 +58,19 @@ class Device:
     def kernel_launches(self) -> int:
         return lib.immx_device_kernel_launches(self.h)
 
+    def profile(self, enable: bool = True):
+        """Bracket the hot kernels with CUDA events on the device stream."""
+        check(lib.immx_device_profile(self.h, int(enable)))
+
+    def reset_stats(self):
+        check(lib.immx_device_reset_stats(self.h))
+
+    def kernel_stats(self, kind: str):
+        """-> {launches, ms, bytes}: device time and ALGORITHMIC bytes of one kernel class."""
+        n, ms, b = C.c_uint64(), C.c_double(), C.c_uint64()
+        check(lib.immx_device_kernel_stats(self.h, _capi.KSTAT[kind], C.byref(n), C.byref(ms), C.byref(b)))
+        return {"launches": n.value, "ms": ms.value, "bytes": b.value}
+
     def __del__(self):
         try:
             if self.h:

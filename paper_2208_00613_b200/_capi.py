@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(HERE, "libimmx_b200.so")
 OK, EINVAL, ERUNTIME, ERANGE, ECUDA = 0, 1, 2, 3, 4
 MODE_HUFFMAN, MODE_BITMAP, MODE_RAW, MODE_AUTO = 0, 1, 2, -1
 MODEL_IC, MODEL_LT = 0, 1
+KSTAT = {"sample": 0, "encode": 1, "hselect": 2, "rselect": 3, "argmax": 4}
 
 P = C.c_void_p
 u8 = C.c_uint8
@@ -79,6 +80,9 @@ SIGNATURES = {
     "immx_device_stream": (P, [P]),
     "immx_device_synchronize": (I, [P]),
     "immx_device_kernel_launches": (u64, [P]),
+    "immx_device_profile": (I, [P, I]),
+    "immx_device_kernel_stats": (I, [P, I, pu64, pdbl, pu64]),
+    "immx_device_reset_stats": (I, [P]),
     "immx_graph_upload": (I, [P, u64, u64, pu64, pu32, pdbl, I, PP]),
     "immx_graph_set_lt_weights": (I, [P, pflt]),
     "immx_graph_info": (I, [P, pu64, pu64, pint]),

@@ -369,6 +369,28 @@ int immx_device_synchronize(immx_device* h) {
     });
 }
 uint64_t immx_device_kernel_launches(const immx_device* h) { return h ? h->d.kernel_launches : 0; }
+int immx_device_profile(immx_device* h, int enable) {
+    return guard([&] {
+        need(h, "device");
+        h->d.profile = enable != 0;
+    });
+}
+int immx_device_kernel_stats(const immx_device* h, int kind, uint64_t* launches, double* ms, uint64_t* bytes) {
+    return guard([&] {
+        need(h, "device");
+        if (kind < 0 || kind >= 8) fail(IMMX_EINVAL, "unknown kernel class");
+        const KStat& s = h->d.kstat[kind];
+        if (launches) *launches = s.launches;
+        if (ms) *ms = s.ms;
+        if (bytes) *bytes = s.bytes;
+    });
+}
+int immx_device_reset_stats(immx_device* h) {
+    return guard([&] {
+        need(h, "device");
+        for (auto& s : h->d.kstat) s = KStat{};
+    });
+}
 
 // ----------------------------------------------------------------- device graph ----
 int immx_graph_upload(immx_device* dv, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt,

@@ -189,10 +189,11 @@ __global__ void k_huff_round(const uint32_t* __restrict__ words, const uint64_t*
                              const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
                              const uint32_t* __restrict__ copied, uint64_t count, const unsigned long long* __restrict__ lut,
                              uint32_t root_bits, const uint32_t* __restrict__ cover_pick, uint8_t* __restrict__ deleted,
-                             unsigned int* __restrict__ hist, unsigned long long* __restrict__ maxdec) {
+                             unsigned int* __restrict__ hist, unsigned long long* __restrict__ maxdec,
+                             unsigned long long* __restrict__ alg_bytes) {
     const uint32_t pick = *cover_pick;
     if (pick == 0xffffffffu) return;
-    uint64_t local_max = 0;
+    uint64_t local_max = 0, local_bytes = 0;
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += (uint64_t)gridDim.x * blockDim.x) {
         if (deleted[j]) continue;
         const uint32_t nbits = bits[j];
@@ -217,7 +218,10 @@ __global__ void k_huff_round(const uint32_t* __restrict__ words, const uint64_t*
                     break;
                 }
         local_max = nd > local_max ? nd : local_max;
+        const uint64_t payload = (nbits + 7) / 8 + 4 * (coff[j + 1] - coff[j]);
+        local_bytes += payload;
         if (found) {
+            local_bytes += payload;  // decoded again to subtract its members
             deleted[j] = 1;
             // the set leaves the live collection: subtract all its members
             br.init(words + woff[j]);
@@ -232,6 +236,7 @@ __global__ void k_huff_round(const uint32_t* __restrict__ words, const uint64_t*
         }
     }
     if (local_max) atomicMax(maxdec, (unsigned long long)local_max);
+    if (local_bytes) atomicAdd(alg_bytes, (unsigned long long)local_bytes);
 }
 
 // decode_find on one set with every reference corruption check (huffman.cpp:129-158)
@@ -350,8 +355,11 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     swap.exact(cnt);
     unsigned long long* d_payload = d.scal.p + 16;
     CK(cudaMemsetAsync(d_payload, 0, 8, s));
+    KTimer kt_size, kt_pack;
+    kt_size.start(&d, IMMX_KSTAT_ENCODE);
     k_enc_size<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_len.p, top,
                                                    S.bits.p + base, nwords.p, ncp.p, swap.p, d_payload);
+    kt_size.stop();
     CK_LAUNCH("k_enc_size");
     d.kernel_launches++;
     // exclusive scans, offset by the running totals: woff[base+1..] = total + inclusive
@@ -379,12 +387,23 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     S.words.reserve(w_total + new_words + 4, s);
     S.copied.reserve(c_total + new_cp + 1, s);
     CK(cudaMemsetAsync(S.words.p + w_total, 0, (new_words + 4) * 4, s));
+    kt_pack.start(&d, IMMX_KSTAT_ENCODE);
     k_enc_pack<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_bits.p, S.code_len.p,
                                                    top, swap.p, S.woff.p + base, S.coff.p + base, S.words.p,
                                                    S.copied.p);
+    kt_pack.stop();
     CK_LAUNCH("k_enc_pack");
     d.kernel_launches++;
     CK(cudaStreamSynchronize(s));
+    {
+        // algorithmic bytes: members read by both passes, payload written once
+        uint64_t members = 0;
+        std::vector<uint32_t> lens(cnt);
+        CK(cudaMemcpy(lens.data(), P.len.p + lo, cnt * 4, cudaMemcpyDeviceToHost));
+        for (uint32_t l : lens) members += l;
+        kt_size.finish(4 * members);
+        kt_pack.finish(4 * members + payload);
+    }
     S.total_words = w_total + new_words;
     S.total_copied = c_total + new_cp;
     S.count = base + cnt;
@@ -472,14 +491,24 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
     ctl.exact(2);  // [0] cover pick, [1] padding flag
     CK(cudaMemsetAsync(ctl.p, 0, 8, s));
     const unsigned grid = grid_for(theta, d);
+    DBuf<unsigned long long> rbytes;
+    rbytes.exact(k);
+    CK(cudaMemsetAsync(rbytes.p, 0, k * 8, s));
+    std::vector<KTimer> kt(k);
     for (uint32_t r = 0; r < k; ++r) {
         argmax_dev(d, d_hist, n, keys.p + r);
         k_pick_from_key<<<1, 1, 0, s>>>(keys.p, r, is_seed.p, seeds.p, marg.p, ctl.p, n, ctl.p + 1);
+        kt[r].start(&d, IMMX_KSTAT_HSELECT);
         k_huff_round<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, theta, S.lut.p,
-                                         S.lut_root_bits, ctl.p, deleted.p, d_hist, mdec.p + r);
+                                         S.lut_root_bits, ctl.p, deleted.p, d_hist, mdec.p + r, rbytes.p + r);
+        kt[r].stop();
         CK_LAUNCH("select_huffman round");
         d.kernel_launches += 2;
     }
+    std::vector<unsigned long long> hbytes(k);
+    CK(cudaMemcpyAsync(hbytes.data(), rbytes.p, k * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (uint32_t r = 0; r < k; ++r) kt[r].finish(hbytes[r] + theta /* deleted flags */);
     std::vector<uint32_t> hseeds(k);
     std::vector<unsigned long long> hmarg(k), hmd(k);
     CK(cudaMemcpyAsync(hseeds.data(), seeds.p, k * 4, cudaMemcpyDeviceToHost, s));

@@ -58,11 +58,30 @@ struct DBuf {
     }
 };
 
+// Per-kernel-class device timing (CUDA events on the launching stream) and algorithmic
+// bytes, for the roofline report.  Classes: IMMX_KSTAT_* in immx_b200.h.
+struct KStat {
+    uint64_t launches = 0;
+    double ms = 0.0;
+    uint64_t bytes = 0;
+};
+struct Device;
+struct KTimer {  // brackets one launch; finish() after the stream was synchronized
+    Device* d = nullptr;
+    int kind = -1;
+    cudaEvent_t a = nullptr, b = nullptr;
+    void start(Device* dev, int k);
+    void stop();
+    void finish(uint64_t bytes);
+};
+
 struct Device {
     int ordinal = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     uint64_t kernel_launches = 0;  // our kernels launched through this context
+    bool profile = false;
+    KStat kstat[8];
     // small scratch
     DBuf<unsigned long long> scal;  // general device scalars
     DBuf<uint8_t> tmp;              // CUB temp storage
@@ -184,6 +203,34 @@ void bitmap_popcount(const BitmapStore& B, unsigned long long* d_hist64);
 void bitmap_row(const BitmapStore& B, uint32_t v, uint32_t* out);
 uint64_t bitmap_subtract_row(BitmapStore& B, uint32_t v, const uint32_t* snap);
 void select_bitmap_dev(BitmapStore& B, unsigned int* d_hist, uint32_t k, SelectOut& out);
+
+inline void KTimer::start(Device* dev, int k) {
+    d = dev;
+    kind = k;
+    if (!d->profile) return;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, d->stream));
+}
+inline void KTimer::stop() {
+    if (d && d->profile && b) CK(cudaEventRecord(b, d->stream));
+}
+inline void KTimer::finish(uint64_t bytes) {
+    if (!d || kind < 0) return;
+    KStat& s = d->kstat[kind];
+    s.launches++;
+    s.bytes += bytes;
+    if (d->profile && a && b) {
+        float ms = 0.f;
+        CK(cudaEventSynchronize(b));
+        CK(cudaEventElapsedTime(&ms, a, b));
+        s.ms += ms;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        a = b = nullptr;
+    }
+    kind = -1;
+}
 
 // ---------------------------------------------------------------- host helpers ----
 struct HostCodebook {

@@ -567,6 +567,8 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         job.nospace_list = nospace.p;
         job.qscratch = qscratch.p;
         job.gbits = gbits.p;
+        KTimer kt;
+        kt.start(&d, IMMX_KSTAT_SAMPLE);
         switch (tier.kind) {
             case kVisSmemBits: launch_tier<kVisSmemBits>(d, gv, job, tier, nitems); break;
             case kVisHash11: launch_tier<kVisHash11>(d, gv, job, tier, nitems); break;
@@ -574,6 +576,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
             case kVisHash15: launch_tier<kVisHash15>(d, gv, job, tier, nitems); break;
             default: launch_tier<kVisGlobBits>(d, gv, job, tier, nitems); break;
         }
+        kt.stop();
         CK(cudaMemcpyAsync(hctl, ctl.p, sizeof(SampCtl), cudaMemcpyDeviceToHost, s));
         unsigned long long cursor = 0;
         CK(cudaMemcpyAsync(&cursor, P.cur.p, 8, cudaMemcpyDeviceToHost, s));
@@ -581,6 +584,12 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         edges += hctl->edges;
         members += hctl->members;
         const uint32_t n_ovf = hctl->n_ovf, n_nospace = hctl->n_nospace;
+        {
+            // algorithmic bytes of the samples this launch committed
+            const uint64_t committed = nitems - n_ovf - n_nospace;
+            const bool edge_bytes = G.pmode == kProbEdge || model == IMMX_MODEL_LT;
+            kt.finish(12ULL * hctl->members + 4ULL * hctl->edges * (edge_bytes ? 2 : 1) + 8ULL * committed);
+        }
         if (n_nospace) {
             // grow the arena past everything reserved so far and redo those samples here
             const uint64_t grow = std::max<uint64_t>((uint64_t)cursor + (uint64_t)(mean * 2.0 * n_nospace) + 65536,
