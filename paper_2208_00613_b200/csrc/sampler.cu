@@ -72,7 +72,9 @@ struct SmemBits {  // n bits in shared memory; never overflows
     static constexpr bool kAlwaysFits = true;
 };
 
-struct GlobBits : SmemBits {};  // same layout, in global memory
+struct GlobBits : SmemBits {  // same layout, in global memory; loads bypass L1
+    __device__ bool has(uint32_t v) const { return (__ldcg(w + (v >> 5)) >> (v & 31)) & 1u; }
+};
 
 template <int LOGH>
 struct SmemHash {  // linear probing, load <= 1/2
@@ -437,15 +439,465 @@ __global__ void __launch_bounds__(256) rrr_kernel(GView g, SampJob job, uint32_t
     }
 }
 
+// ============================================================ block-cooperative IC ====
+// One CTA (NW warps) owns one sample; the visited set is shared by the CTA.  The flattened
+// edge sequence of a batch of up to NW*32 rows is consumed in groups of G = NW*32*U edges:
+// position p = gpos + (warp*U + i)*32 + lane.  Per group:
+//   1. every lane loads its edge, tests the visited snapshot, ballots "draws";
+//   2. a CTA prefix over the warps' draw counts gives each lane its draw number, so the
+//      coins are computed independently (branch-free, U per lane);
+//   3. successes are inserted; a group that spans several rows may repeat a target -- a
+//      repeated success or a failed candidate whose target a success just inserted is
+//      flagged (__syncthreads_or).  Flagged groups (rare) are resolved exactly: the first
+//      position whose target repeats an earlier success is the cut; the group commits up to
+//      the cut and the visited set is rebuilt from the committed members.
+// Successes are appended in position order, which is the reference's member order.
+struct BBits {  // CTA-shared bitmap over all n vertices (smem or a per-CTA global slice)
+    uint32_t* w;
+    uint32_t words;
+    __device__ bool has(uint32_t v) const { return (w[v >> 5] >> (v & 31)) & 1u; }
+    __device__ bool add_test(uint32_t v) { return atomicOr(&w[v >> 5], 1u << (v & 31)) & (1u << (v & 31)); }
+    __device__ void clear_all() {
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) w[i] = 0;
+    }
+    __device__ void clear_members(const uint32_t* q, uint32_t len) {
+        if (len > words / 8) clear_all();
+        else
+            for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) w[q[i] >> 5] = 0;
+    }
+};
+
+struct BGBits : BBits {  // global-memory bitmap: loads bypass L1 (atomics live in L2)
+    __device__ bool has(uint32_t v) const { return (__ldcg(w + (v >> 5)) >> (v & 31)) & 1u; }
+};
+
+template <int LOGH>
+struct BHash {  // CTA-shared linear-probing hash, load <= 1/2
+    uint32_t* s;
+    static constexpr uint32_t H = 1u << LOGH;
+    __device__ static uint32_t h(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - LOGH); }
+    __device__ bool has(uint32_t v) const {
+        uint32_t i = h(v);
+        for (;;) {
+            const uint32_t k = s[i];
+            if (k == v) return true;
+            if (k == kEmptyKey) return false;
+            i = (i + 1) & (H - 1);
+        }
+    }
+    __device__ bool add_test(uint32_t v) {
+        uint32_t i = h(v);
+        for (;;) {
+            const uint32_t old = atomicCAS(&s[i], kEmptyKey, v);
+            if (old == kEmptyKey) return false;
+            if (old == v) return true;
+            i = (i + 1) & (H - 1);
+        }
+    }
+    __device__ void clear_all() {
+        const uint4 e = make_uint4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
+        for (uint32_t i = threadIdx.x; i < H / 4; i += blockDim.x) reinterpret_cast<uint4*>(s)[i] = e;
+    }
+    __device__ void clear_members(const uint32_t*, uint32_t) { clear_all(); }
+};
+
+enum BVisKind { kBBits = 0, kBHash13 = 1, kBHash15 = 2, kBGlob = 3 };
+template <int K>
+struct BVisOf;
+template <>
+struct BVisOf<kBBits> { using T = BBits; };
+template <>
+struct BVisOf<kBHash13> { using T = BHash<13>; };
+template <>
+struct BVisOf<kBHash15> { using T = BHash<15>; };
+template <>
+struct BVisOf<kBGlob> { using T = BGBits; };
+
+template <int NW, int U>
+struct BlkSmem {
+    uint64_t rs[NW * 32];    // col index of flattened position 0 of the row (row start - exclusive cum)
+    uint32_t cum[NW * 32];   // inclusive prefix of the batch's row degrees
+    uint64_t thr[NW * 32];   // row threshold (global / per-row modes)
+    alignas(16) uint32_t wsum[NW];
+    alignas(16) uint32_t wsum2[NW];
+    uint32_t wrow[NW];  // per warp: first row << 16 | last row of its slice of the group
+    uint32_t lpos[NW * 32 * U];  // rare path: success positions
+    uint32_t lv[NW * 32 * U];    //            and targets
+    uint32_t cut;
+    uint32_t j;
+    unsigned long long base;
+};
+
+template <int NW>
+__device__ __forceinline__ uint32_t find_row(const uint32_t* cum, uint32_t e) {
+    // smallest r with cum[r] > e (cum is non-decreasing over NW*32 entries)
+    uint32_t lo = 0, hi = NW * 32 - 1;
+#pragma unroll
+    for (int s = 0; (1 << s) < NW * 32; ++s) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cum[mid] > e) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+// sum of the first `w` entries and of all NW entries of a per-warp smem array
+template <int NW>
+__device__ __forceinline__ void warp_prefix(const uint32_t* a, uint32_t w, uint32_t& before, uint32_t& total) {
+    static_assert(NW % 4 == 0, "NW must be a multiple of 4");
+    before = 0;
+    total = 0;
+#pragma unroll
+    for (int k = 0; k < NW; k += 4) {
+        const uint4 x = *reinterpret_cast<const uint4*>(a + k);
+        before += ((uint32_t)k < w ? x.x : 0u) + ((uint32_t)k + 1 < w ? x.y : 0u) + ((uint32_t)k + 2 < w ? x.z : 0u) +
+                  ((uint32_t)k + 3 < w ? x.w : 0u);
+        total += x.x + x.y + x.z + x.w;
+    }
+}
+
+template <int KIND, int PM, int NW, int U>
+__global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob job, uint32_t vis_words) {
+    extern __shared__ uint32_t dsm[];
+    __shared__ BlkSmem<NW, U> sh;
+    constexpr uint32_t NB = NW * 32;
+    constexpr uint32_t G = NW * 32 * U;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t lt = lanemask_lt();
+    uint32_t* q = job.qscratch + (size_t)blockIdx.x * job.qcap;
+    typename BVisOf<KIND>::T vis;
+    if constexpr (KIND == kBBits) {
+        vis.w = dsm;
+        vis.words = vis_words;
+    } else if constexpr (KIND == kBGlob) {
+        vis.w = job.gbits + (size_t)blockIdx.x * vis_words;
+        vis.words = vis_words;
+    } else {
+        vis.s = dsm;
+    }
+    if constexpr (KIND != kBGlob) vis.clear_all();  // the host zeroes global bitmaps
+    __syncthreads();
+    for (;;) {
+        if (tid == 0) {
+            sh.j = atomicAdd(&job.ctl->work, 1u);
+            // arena exhausted: hand the sample back untouched (the host grows the arena)
+            sh.cut = atomicAdd(job.cursor, 0ULL) >= job.arena_cap ? 1u : 0u;
+        }
+        __syncthreads();
+        const uint32_t idx = sh.j;
+        if (idx >= job.count) break;
+        const uint32_t j = job.list ? job.list[idx] : idx;
+        if (sh.cut) {
+            if (tid == 0) job.nospace_list[atomicAdd(&job.ctl->n_nospace, 1u)] = j;
+            __syncthreads();
+            continue;
+        }
+        uint64_t s0, t;
+        uint32_t root;
+        if (job.roots) {
+            s0 = job.states[j];
+            root = job.roots[j];
+            t = 1;
+        } else {
+            s0 = stream_state(job.seed, job.first + j);
+            root = (uint32_t)below(draw(s0, 1), g.n);
+            t = 2;
+        }
+        if (tid == 0) {
+            q[0] = root;
+            vis.add_test(root);
+        }
+        uint32_t qhead = 0, qlen = 1;
+        uint64_t edges = 0;
+        bool overflow = false;
+        __syncthreads();
+        while (qhead < qlen && !overflow) {
+            // ---- batch of rows q[qhead .. qhead+nb) ----
+            const uint32_t nb = min(NB, qlen - qhead);
+            uint32_t deg = 0;
+            uint64_t rs = 0, th = g.gthr;
+            if (tid < nb) {
+                const uint32_t u = q[qhead + tid];
+                rs = g.row[u];
+                deg = (uint32_t)(g.row[u + 1] - rs);
+                if (PM == kProbRow) th = g.thr[u];
+            }
+            uint32_t x = deg;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            if (lane == 31) sh.wsum[w] = x;
+            __syncthreads();
+            uint32_t off, total;
+            warp_prefix<NW>(sh.wsum, w, off, total);
+            sh.cum[tid] = x + off;
+            sh.rs[tid] = rs - (uint64_t)(x + off - deg);  // col index of flattened position p = rs + p
+            if (PM == kProbRow) sh.thr[tid] = th;
+            __syncthreads();
+            edges += total;
+            qhead += nb;
+            uint32_t gpos = 0;
+            uint32_t r_w = 0;  // row holding this warp's first position (monotone over the batch)
+            uint32_t r_g = 0;  // row holding gpos (monotone over the batch)
+            while (gpos < total) {
+                // ---- one group: positions gpos + (w*U + i)*32 + lane ----
+                uint32_t v[U];
+                uint64_t T[U];
+                bool cand[U];
+                uint32_t dm[U];
+                uint32_t wd = 0;
+                const uint32_t a0 = gpos + w * U * 32;
+                const uint32_t a0c = min(a0, total - 1);
+                while (sh.cum[r_w] <= a0c) ++r_w;
+                while (sh.cum[r_g] <= gpos) ++r_g;
+                uint32_t r_last = r_g;  // row of this warp's last valid edge
+                if (a0 < total && sh.cum[r_w] >= min(a0 + U * 32, total)) {
+                    // fast path: the warp's whole slice lies in row r_w
+                    const uint64_t base = sh.rs[r_w];
+                    const uint64_t Trow = PM == kProbRow ? sh.thr[r_w] : g.gthr;
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        const uint32_t e = a0 + i * 32 + lane;
+                        const bool valid = e < total;
+                        v[i] = valid ? __ldg(g.col + base + e) : 0u;
+                        if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + base + e) : 0ull;
+                        else T[i] = Trow;
+                    }
+                    r_last = r_w;
+                } else {
+                    // the slice crosses rows: per sub-window, a 5-step search for lanes that need it
+                    uint32_t r = r_w;
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        const uint32_t a = a0 + i * 32;
+                        const uint32_t e = a + lane;
+                        const bool valid = e < total;
+                        const uint32_t ec = min(e, total - 1);
+                        while (sh.cum[r] <= min(a, total - 1)) ++r;
+                        uint32_t rr = r;
+                        if (a < total && sh.cum[r] < min(a + 32, total)) {
+                            uint32_t lo = r, hi = min(r + 31, NB - 1);
+#pragma unroll
+                            for (int s = 0; s < 5; ++s) {
+                                const uint32_t mid = (lo + hi) >> 1;
+                                if (sh.cum[mid] > ec) hi = mid;
+                                else lo = mid + 1;
+                            }
+                            rr = lo;
+                        }
+                        r = __shfl_sync(FULL, rr, 31);
+                        if (a < total) r_last = __shfl_sync(FULL, rr, min(total - 1 - a, 31u));
+                        const uint64_t eg = sh.rs[rr] + (uint64_t)ec;
+                        v[i] = valid ? __ldg(g.col + eg) : 0u;
+                        if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + eg) : 0ull;
+                        else if (PM == kProbRow) T[i] = sh.thr[rr];
+                        else T[i] = g.gthr;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < U; ++i) {
+                    const bool valid = a0 + i * 32 + lane < total;
+                    cand[i] = valid && T[i] != kThrNever && !vis.has(v[i]);
+                    dm[i] = __ballot_sync(FULL, cand[i] && T[i] != kThrAlways);
+                    wd += __popc(dm[i]);
+                }
+                if (lane == 0) sh.wsum[w] = wd;
+                // barrier + "does the group span several rows" in one instruction
+                const bool multi = __syncthreads_or(r_last != r_g) || g.row_dups;
+                uint32_t dbefore, dtotal;
+                warp_prefix<NW>(sh.wsum, w, dbefore, dtotal);
+                bool succ[U];
+                uint32_t sm[U];
+                uint32_t ws = 0;
+                uint64_t tb = t + dbefore;
+#pragma unroll
+                for (int i = 0; i < U; ++i) {
+                    const bool coin = coin_success(s0, tb + __popc(dm[i] & lt), T[i]);  // branch-free
+                    succ[i] = cand[i] && (T[i] == kThrAlways || coin);
+                    tb += __popc(dm[i]);
+                    sm[i] = __ballot_sync(FULL, succ[i]);
+                    ws += __popc(sm[i]);
+                }
+                if (lane == 0) sh.wsum2[w] = ws;
+                __syncthreads();
+                uint32_t sbefore, stotal;
+                warp_prefix<NW>(sh.wsum2, w, sbefore, stotal);
+                // the sample outgrows this tier (hash tiers only: a bitmap tier holds all n, and
+                // stotal may count a repeated target twice): restart it on the next tier
+                if (job.qcap < g.n && qlen + stotal > job.qcap) {
+                    overflow = true;
+                    break;
+                }
+                bool flag = false;
+#pragma unroll
+                for (int i = 0; i < U; ++i)
+                    if (succ[i]) flag |= vis.add_test(v[i]);
+                __syncthreads();
+                if (multi) {
+#pragma unroll
+                    for (int i = 0; i < U; ++i)
+                        if (cand[i] && !succ[i] && vis.has(v[i])) flag = true;
+                }
+                if (!__syncthreads_or(flag)) {
+                    // common case: commit the whole group
+                    uint32_t p = qlen + sbefore;
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        if (succ[i]) q[p + __popc(sm[i] & lt)] = v[i];
+                        p += __popc(sm[i]);
+                    }
+                    qlen += stotal;
+                    t += dtotal;
+                    gpos += G;
+                } else {
+                    // rare: resolve the first position whose target repeats an earlier success
+                    {
+                        uint32_t p = sbefore;
+#pragma unroll
+                        for (int i = 0; i < U; ++i) {
+                            if (succ[i]) {
+                                const uint32_t k = p + __popc(sm[i] & lt);
+                                sh.lpos[k] = gpos + (w * U + i) * 32 + lane;
+                                sh.lv[k] = v[i];
+                            }
+                            p += __popc(sm[i]);
+                        }
+                    }
+                    if (tid == 0) sh.cut = 0xffffffffu;
+                    __syncthreads();
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        if (!cand[i] || !vis.has(v[i])) continue;
+                        const uint32_t pos = gpos + (w * U + i) * 32 + lane;
+                        uint32_t minp = 0xffffffffu;
+                        for (uint32_t k = 0; k < stotal; ++k)
+                            if (sh.lv[k] == v[i]) minp = min(minp, sh.lpos[k]);
+                        if (minp < pos) atomicMin(&sh.cut, pos);
+                    }
+                    __syncthreads();
+                    const uint32_t cut = sh.cut;
+                    // counts of draws / successes before the cut
+                    uint32_t wd2 = 0, ws2 = 0;
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        const uint32_t a = gpos + (w * U + i) * 32;
+                        const uint32_t keep = cut == 0xffffffffu ? FULL
+                                            : (cut <= a ? 0u : (cut - a >= 32 ? FULL : ((1u << (cut - a)) - 1u)));
+                        wd2 += __popc(dm[i] & keep);
+                        ws2 += __popc(sm[i] & keep);
+                        sm[i] &= keep;
+                    }
+                    __syncthreads();
+                    if (lane == 0) {
+                        sh.wsum[w] = wd2;
+                        sh.wsum2[w] = ws2;
+                    }
+                    __syncthreads();
+                    uint32_t d2b = 0, d2t = 0, s2b = 0, s2t = 0;
+#pragma unroll
+                    for (int k = 0; k < NW; ++k) {
+                        const uint32_t c = sh.wsum[k], c2 = sh.wsum2[k];
+                        d2b += (uint32_t)k < w ? c : 0u;
+                        d2t += c;
+                        s2b += (uint32_t)k < w ? c2 : 0u;
+                        s2t += c2;
+                    }
+                    uint32_t p = qlen + s2b;
+#pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        if ((sm[i] >> lane) & 1u) q[p + __popc(sm[i] & lt)] = v[i];
+                        p += __popc(sm[i]);
+                    }
+                    qlen += s2t;
+                    t += d2t;
+                    gpos = cut == 0xffffffffu ? gpos + G : cut;
+                    if (cut != 0xffffffffu) {
+                        // rebuild the visited set from the committed members
+                        __syncthreads();
+                        vis.clear_all();
+                        __syncthreads();
+                        for (uint32_t k = tid; k < qlen; k += blockDim.x) vis.add_test(q[k]);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+        if (!overflow) {
+            if (tid == 0) sh.base = atomicAdd(job.cursor, (unsigned long long)qlen);
+            __syncthreads();
+            const unsigned long long base = sh.base;
+            if (base + qlen > job.arena_cap) {
+                if (tid == 0) job.nospace_list[atomicAdd(&job.ctl->n_nospace, 1u)] = j;
+            } else {
+                for (uint32_t k = tid; k < qlen; k += blockDim.x) job.arena[base + k] = q[k];
+                if (tid == 0) {
+                    job.set_off[job.pool_base + j] = base;
+                    job.set_len[job.pool_base + j] = qlen;
+                    atomicAdd(&job.ctl->edges, (unsigned long long)edges);
+                    atomicAdd(&job.ctl->members, (unsigned long long)qlen);
+                }
+            }
+        } else if (tid == 0) {
+            job.ovf_list[atomicAdd(&job.ctl->n_ovf, 1u)] = j;
+        }
+        __syncthreads();
+        vis.clear_members(q, qlen);
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------- host side ----
 namespace {
 
 struct Tier {
     int kind;
-    uint32_t smem_words_per_warp;  // 0 for global tiers
+    uint32_t smem_words_per_warp;  // 0 for global tiers (block tiers: words per CTA)
     uint32_t warps_per_block;
     uint32_t qcap;
+    bool block = false;            // CTA-cooperative kernel
+    uint32_t max_blocks = 0;       // 0 = occupancy-limited
 };
+
+constexpr int kBlkNW = 8;
+constexpr int kBlkU = 4;
+
+template <int KIND>
+uint32_t block_grid(Device& d, const Tier& tier, size_t smem) {
+    for (auto kern : {rrr_block_kernel<KIND, kProbGlobal, kBlkNW, kBlkU>, rrr_block_kernel<KIND, kProbRow, kBlkNW, kBlkU>,
+                      rrr_block_kernel<KIND, kProbEdge, kBlkNW, kBlkU>}) {
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
+    auto kern = rrr_block_kernel<KIND, kProbEdge, kBlkNW, kBlkU>;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlkNW * 32, smem));
+    if (per_sm < 1) fail(IMMX_ECUDA, "sampler tier does not fit on an SM");
+    uint32_t blocks = (uint32_t)per_sm * (uint32_t)d.num_sms;
+    if (tier.max_blocks) blocks = std::min(blocks, tier.max_blocks);
+    return blocks;
+}
+
+template <int KIND>
+void launch_block_tier(Device& d, const GView& gv, SampJob job, const Tier& tier, uint32_t nitems, uint32_t blocks) {
+    const size_t smem = (size_t)tier.smem_words_per_warp * 4;
+    blocks = std::min<uint32_t>(blocks, std::max<uint32_t>(1, nitems));
+    job.qcap = tier.qcap;
+    if (gv.pmode == kProbGlobal)
+        rrr_block_kernel<KIND, kProbGlobal, kBlkNW, kBlkU><<<blocks, kBlkNW * 32, smem, d.stream>>>(
+            gv, job, tier.smem_words_per_warp);
+    else if (gv.pmode == kProbRow)
+        rrr_block_kernel<KIND, kProbRow, kBlkNW, kBlkU><<<blocks, kBlkNW * 32, smem, d.stream>>>(
+            gv, job, tier.smem_words_per_warp);
+    else
+        rrr_block_kernel<KIND, kProbEdge, kBlkNW, kBlkU><<<blocks, kBlkNW * 32, smem, d.stream>>>(
+            gv, job, tier.smem_words_per_warp);
+    CK_LAUNCH("rrr_block_kernel");
+    d.kernel_launches++;
+}
 
 template <int KIND>
 void launch_tier(Device& d, const GView& gv, SampJob job, const Tier& tier, uint32_t nitems) {
@@ -497,11 +949,19 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     if (count > 0xffffffffULL) fail(IMMX_EINVAL, "sample batch larger than 2^32");
     if (G.n == 0) fail(IMMX_EINVAL, "graph has no vertices");
     if (model == IMMX_MODEL_LT && !G.has_lt) fail(IMMX_EINVAL, "LT model requires per-edge LT weights");
+    if (P.count < 1024 && count > 8192) {
+        // cold pool: a pilot batch measures the mean set size, so the arena is sized once
+        // (an undersized arena makes in-flight samples redo their work)
+        sample_into_pool(P, G, 2048, first, seed, d_roots, d_states, model);
+        sample_into_pool(P, G, count - 2048, first + 2048, seed, d_roots ? d_roots + 2048 : nullptr,
+                         d_states ? d_states + 2048 : nullptr, model);
+        return;
+    }
     const uint64_t base = P.count;
     P.off.reserve(base + count, s);
     P.len.reserve(base + count, s);
-    // arena: grow to an estimate (mean size so far, else 8 per sample)
-    const double mean = P.count ? (double)P.members / (double)P.count : 8.0;
+    // arena: grow to an estimate (mean size so far, else 64 per sample)
+    const double mean = P.count ? (double)P.members / (double)P.count : (double)std::min<uint64_t>(G.n, 4096);
     const uint64_t want = P.arena_used + (uint64_t)(mean * 1.25 * (double)count) + 4096;
     P.arena.reserve(want, s);
     P.cur.reserve(1, s);
@@ -510,7 +970,18 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     // tiers
     std::vector<Tier> tiers;
     const uint64_t nwords = (G.n + 31) / 32;
-    if (nwords * 4 <= 40 * 1024) {
+    const uint32_t ncap = (uint32_t)std::min<uint64_t>(G.n, 0xffffffffu);
+    if (model == IMMX_MODEL_IC) {
+        // CTA-cooperative tiers: a CTA-shared bitmap when n/8 <= 64 KB, else CTA-shared hashes
+        // escalating to a per-CTA global bitmap
+        if (nwords * 4 <= 64 * 1024) {
+            tiers.push_back({kBBits, (uint32_t)nwords, kBlkNW, ncap, true, 0});
+        } else {
+            tiers.push_back({kBHash13, 1u << 13, kBlkNW, 1u << 12, true, 0});
+            tiers.push_back({kBHash15, 1u << 15, kBlkNW, 1u << 14, true, 0});
+            tiers.push_back({kBGlob, 0, kBlkNW, ncap, true, 64});
+        }
+    } else if (nwords * 4 <= 40 * 1024) {
         const uint32_t bytes = (uint32_t)(nwords * 4);
         uint32_t wpb = 8;
         while (wpb > 1 && (uint64_t)bytes * wpb > 100 * 1024) wpb /= 2;
@@ -552,9 +1023,20 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     unsigned long long edges = 0, members = 0;
     for (size_t ti = 0; ti < tiers.size() && nitems > 0;) {
         const Tier& tier = tiers[ti];
-        const uint32_t warps = grid_warps(d, tier);
+        uint32_t warps = 0;  // warps (warp tiers) or CTAs (block tiers) that may run
+        if (tier.block) {
+            const size_t smem = (size_t)tier.smem_words_per_warp * 4;
+            switch (tier.kind) {
+                case kBBits: warps = block_grid<kBBits>(d, tier, smem); break;
+                case kBHash13: warps = block_grid<kBHash13>(d, tier, smem); break;
+                case kBHash15: warps = block_grid<kBHash15>(d, tier, smem); break;
+                default: warps = block_grid<kBGlob>(d, tier, smem); break;
+            }
+        } else {
+            warps = grid_warps(d, tier);
+        }
         qscratch.reserve((uint64_t)warps * tier.qcap, s, false);
-        if (tier.kind == kVisGlobBits) {
+        if ((tier.block && tier.kind == kBGlob) || (!tier.block && tier.kind == kVisGlobBits)) {
             gbits.reserve((uint64_t)warps * nwords, s, false);
             CK(cudaMemsetAsync(gbits.p, 0, (size_t)warps * nwords * 4, s));
         }
@@ -569,12 +1051,21 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         job.gbits = gbits.p;
         KTimer kt;
         kt.start(&d, IMMX_KSTAT_SAMPLE);
-        switch (tier.kind) {
-            case kVisSmemBits: launch_tier<kVisSmemBits>(d, gv, job, tier, nitems); break;
-            case kVisHash11: launch_tier<kVisHash11>(d, gv, job, tier, nitems); break;
-            case kVisHash13: launch_tier<kVisHash13>(d, gv, job, tier, nitems); break;
-            case kVisHash15: launch_tier<kVisHash15>(d, gv, job, tier, nitems); break;
-            default: launch_tier<kVisGlobBits>(d, gv, job, tier, nitems); break;
+        if (tier.block) {
+            switch (tier.kind) {
+                case kBBits: launch_block_tier<kBBits>(d, gv, job, tier, nitems, warps); break;
+                case kBHash13: launch_block_tier<kBHash13>(d, gv, job, tier, nitems, warps); break;
+                case kBHash15: launch_block_tier<kBHash15>(d, gv, job, tier, nitems, warps); break;
+                default: launch_block_tier<kBGlob>(d, gv, job, tier, nitems, warps); break;
+            }
+        } else {
+            switch (tier.kind) {
+                case kVisSmemBits: launch_tier<kVisSmemBits>(d, gv, job, tier, nitems); break;
+                case kVisHash11: launch_tier<kVisHash11>(d, gv, job, tier, nitems); break;
+                case kVisHash13: launch_tier<kVisHash13>(d, gv, job, tier, nitems); break;
+                case kVisHash15: launch_tier<kVisHash15>(d, gv, job, tier, nitems); break;
+                default: launch_tier<kVisGlobBits>(d, gv, job, tier, nitems); break;
+            }
         }
         kt.stop();
         CK(cudaMemcpyAsync(hctl, ctl.p, sizeof(SampCtl), cudaMemcpyDeviceToHost, s));
@@ -592,8 +1083,10 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         }
         if (n_nospace) {
             // grow the arena past everything reserved so far and redo those samples here
-            const uint64_t grow = std::max<uint64_t>((uint64_t)cursor + (uint64_t)(mean * 2.0 * n_nospace) + 65536,
-                                                     P.arena.cap + P.arena.cap / 2);
+            const uint64_t committed = nitems - n_ovf - n_nospace;
+            const double obs = committed ? (double)hctl->members / (double)committed : mean;
+            const uint64_t grow = std::max<uint64_t>(
+                (uint64_t)cursor + (uint64_t)(std::max(obs, mean) * 1.3 * n_nospace) + 65536, P.arena.cap * 2);
             P.arena.reserve(grow, s);
             // merge: the nospace samples go first through the same tier again
             CK(cudaMemcpyAsync(lists[in_buf ^ 1].p + n_ovf, nospace.p, (size_t)n_nospace * 4,
