@@ -541,6 +541,19 @@ __device__ __forceinline__ uint32_t find_row(const uint32_t* cum, uint32_t e) {
     return lo;
 }
 
+// row holding flattened position x, searching forward from row r (cum is non-decreasing)
+template <int NW>
+__device__ __forceinline__ uint32_t advance_row(const uint32_t* cum, uint32_t r, uint32_t x) {
+    if (cum[r] > x) return r;
+    uint32_t lo = r + 1, hi = NW * 32 - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (cum[mid] > x) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
 // sum of the first `w` entries and of all NW entries of a per-warp smem array
 template <int NW>
 __device__ __forceinline__ void warp_prefix(const uint32_t* a, uint32_t w, uint32_t& before, uint32_t& total) {
@@ -640,7 +653,6 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
             qhead += nb;
             uint32_t gpos = 0;
             uint32_t r_w = 0;  // row holding this warp's first position (monotone over the batch)
-            uint32_t r_g = 0;  // row holding gpos (monotone over the batch)
             while (gpos < total) {
                 // ---- one group: positions gpos + (w*U + i)*32 + lane ----
                 uint32_t v[U];
@@ -650,10 +662,11 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                 uint32_t wd = 0;
                 const uint32_t a0 = gpos + w * U * 32;
                 const uint32_t a0c = min(a0, total - 1);
-                while (sh.cum[r_w] <= a0c) ++r_w;
-                while (sh.cum[r_g] <= gpos) ++r_g;
-                uint32_t r_last = r_g;  // row of this warp's last valid edge
+                r_w = advance_row<NW>(sh.cum, r_w, a0c);
+                // this warp's slice leaves the row holding gpos -> the group spans several rows
+                bool my_multi = false;
                 if (a0 < total && sh.cum[r_w] >= min(a0 + U * 32, total)) {
+                    my_multi = r_w && sh.cum[r_w - 1] > gpos;
                     // fast path: the warp's whole slice lies in row r_w
                     const uint64_t base = sh.rs[r_w];
                     const uint64_t Trow = PM == kProbRow ? sh.thr[r_w] : g.gthr;
@@ -665,9 +678,9 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                         if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + base + e) : 0ull;
                         else T[i] = Trow;
                     }
-                    r_last = r_w;
                 } else {
                     // the slice crosses rows: per sub-window, a 5-step search for lanes that need it
+                    my_multi = a0 < total;
                     uint32_t r = r_w;
 #pragma unroll
                     for (int i = 0; i < U; ++i) {
@@ -675,7 +688,7 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                         const uint32_t e = a + lane;
                         const bool valid = e < total;
                         const uint32_t ec = min(e, total - 1);
-                        while (sh.cum[r] <= min(a, total - 1)) ++r;
+                        r = advance_row<NW>(sh.cum, r, min(a, total - 1));
                         uint32_t rr = r;
                         if (a < total && sh.cum[r] < min(a + 32, total)) {
                             uint32_t lo = r, hi = min(r + 31, NB - 1);
@@ -688,7 +701,6 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                             rr = lo;
                         }
                         r = __shfl_sync(FULL, rr, 31);
-                        if (a < total) r_last = __shfl_sync(FULL, rr, min(total - 1 - a, 31u));
                         const uint64_t eg = sh.rs[rr] + (uint64_t)ec;
                         v[i] = valid ? __ldg(g.col + eg) : 0u;
                         if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + eg) : 0ull;
@@ -705,7 +717,7 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                 }
                 if (lane == 0) sh.wsum[w] = wd;
                 // barrier + "does the group span several rows" in one instruction
-                const bool multi = __syncthreads_or(r_last != r_g) || g.row_dups;
+                const bool multi = __syncthreads_or(my_multi) || g.row_dups;
                 uint32_t dbefore, dtotal;
                 warp_prefix<NW>(sh.wsum, w, dbefore, dtotal);
                 bool succ[U];
@@ -721,26 +733,39 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                     ws += __popc(sm[i]);
                 }
                 if (lane == 0) sh.wsum2[w] = ws;
+                // Insert the successes before the barrier (which then also publishes them) when
+                // the visited set cannot overflow: bitmap tiers hold all n; a hash tier has room
+                // for a whole group.  Otherwise check the capacity first (stotal may count a
+                // repeated target twice -- then the sample just moves to the next tier).
+                const bool early = KIND == kBBits || KIND == kBGlob || qlen + G <= job.qcap;
+                bool flag = false;
+                if (early) {
+#pragma unroll
+                    for (int i = 0; i < U; ++i)
+                        if (succ[i]) flag |= vis.add_test(v[i]);
+                }
                 __syncthreads();
                 uint32_t sbefore, stotal;
                 warp_prefix<NW>(sh.wsum2, w, sbefore, stotal);
-                // the sample outgrows this tier (hash tiers only: a bitmap tier holds all n, and
-                // stotal may count a repeated target twice): restart it on the next tier
-                if (job.qcap < g.n && qlen + stotal > job.qcap) {
-                    overflow = true;
-                    break;
-                }
-                bool flag = false;
+                if (!early) {
+                    if (qlen + stotal > job.qcap) {
+                        overflow = true;
+                        break;
+                    }
 #pragma unroll
-                for (int i = 0; i < U; ++i)
-                    if (succ[i]) flag |= vis.add_test(v[i]);
-                __syncthreads();
+                    for (int i = 0; i < U; ++i)
+                        if (succ[i]) flag |= vis.add_test(v[i]);
+                    __syncthreads();
+                }
+                // a single-row group has distinct targets: no success can repeat a target
+                bool conflict = false;
                 if (multi) {
 #pragma unroll
                     for (int i = 0; i < U; ++i)
                         if (cand[i] && !succ[i] && vis.has(v[i])) flag = true;
+                    conflict = __syncthreads_or(flag);
                 }
-                if (!__syncthreads_or(flag)) {
+                if (!conflict) {
                     // common case: commit the whole group
                     uint32_t p = qlen + sbefore;
 #pragma unroll
@@ -812,17 +837,31 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                     }
                     qlen += s2t;
                     t += d2t;
-                    gpos = cut == 0xffffffffu ? gpos + G : cut;
                     if (cut != 0xffffffffu) {
-                        // rebuild the visited set from the committed members
-                        __syncthreads();
-                        vis.clear_all();
-                        __syncthreads();
-                        for (uint32_t k = tid; k < qlen; k += blockDim.x) vis.add_test(q[k]);
+                        if constexpr (KIND == kBBits || KIND == kBGlob) {
+                            // roll back the successes at or after the cut, then restore the
+                            // committed ones (a repeated target may have shared a bit)
+#pragma unroll
+                            for (int i = 0; i < U; ++i)
+                                if (succ[i] && gpos + (w * U + i) * 32 + lane >= cut)
+                                    atomicAnd(&vis.w[v[i] >> 5], ~(1u << (v[i] & 31)));
+                            __syncthreads();
+#pragma unroll
+                            for (int i = 0; i < U; ++i)
+                                if ((sm[i] >> lane) & 1u) vis.add_test(v[i]);
+                        } else {
+                            // rebuild the visited set from the committed members
+                            __syncthreads();
+                            vis.clear_all();
+                            __syncthreads();
+                            for (uint32_t k = tid; k < qlen; k += blockDim.x) vis.add_test(q[k]);
+                        }
                     }
+                    gpos = cut == 0xffffffffu ? gpos + G : cut;
+                    __syncthreads();  // rare path: rebuilt visited set, smem success list reuse
                 }
-                __syncthreads();
             }
+            __syncthreads();  // the batch's queue writes before the next batch reads them
         }
         __syncthreads();
         if (!overflow) {
