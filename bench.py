@@ -290,12 +290,15 @@ def run_ours(args, cfg, rank, world, local):
     r0 = results[-1]
     peak, peak_kind = load_peaks()
     samp_gbs = samp["bytes"] / (samp["ms"] / 1000.0) / 1e9 if samp["ms"] else None
+    # DRAM bytes per launch: the dram/algorithmic ratio of the ncu --set full capture of the
+    # same kernel on this config (profiles/), applied to this run's bytes per launch
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_sampler_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(args.config)
+                ratio = json.load(f)[args.config]["dram_over_alg"]
+            traffic = ratio * samp["bytes"] / max(samp["launches"], 1)
         except Exception:
             traffic = None
 

@@ -349,6 +349,11 @@ int immx_device_create(int ordinal, immx_device** out) {
         d.ordinal = ordinal;
         CK(cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, ordinal));
         CK(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+        alloc_stream() = d.stream;
+        cudaMemPool_t mp;
+        CK(cudaDeviceGetDefaultMemPool(&mp, ordinal));
+        uint64_t keep_all = ~0ULL;  // keep freed memory in the pool for the next run
+        CK(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep_all));
         d.scal.exact(64);
         CK(cudaMallocHost(&d.host_scal, 64 * 8));
         *out = h;
@@ -358,6 +363,10 @@ void immx_device_destroy(immx_device* h) {
     if (!h) return;
     cudaStreamSynchronize(h->d.stream);
     if (h->d.host_scal) cudaFreeHost(h->d.host_scal);
+    h->d.scal.release();
+    h->d.tmp.release();
+    if (alloc_stream() == h->d.stream) alloc_stream() = nullptr;  // objects outliving it free on stream 0
+    cudaStreamSynchronize(h->d.stream);
     cudaStreamDestroy(h->d.stream);
     delete h;
 }

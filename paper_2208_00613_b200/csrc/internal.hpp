@@ -25,6 +25,15 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define CK(x) ::immx_dev::cuda_check((x), #x)
 #define CK_LAUNCH(what) ::immx_dev::cuda_check(cudaGetLastError(), what)
 
+// The stream all device allocations are ordered on (the immx_device stream; one device
+// context per process is the supported configuration).  Allocation goes through the
+// stream-ordered pool (cudaMallocAsync), whose release threshold is raised at device
+// creation, so repeated runs reuse memory instead of paying cudaMalloc/cudaFree.
+inline cudaStream_t& alloc_stream() {
+    static cudaStream_t s = nullptr;
+    return s;
+}
+
 // A growable device buffer (never shrinks; contents preserved on growth).
 template <class T>
 struct DBuf {
@@ -32,7 +41,7 @@ struct DBuf {
     uint64_t cap = 0;
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, alloc_stream());
         p = nullptr;
         cap = 0;
     }
@@ -41,19 +50,16 @@ struct DBuf {
         uint64_t nc = cap ? cap : 1024;
         while (nc < n) nc += nc / 2 + 1024;
         T* q = nullptr;
-        CK(cudaMalloc(&q, nc * sizeof(T)));
+        CK(cudaMallocAsync(&q, nc * sizeof(T), alloc_stream()));
         if (keep && p && cap) CK(cudaMemcpyAsync(q, p, cap * sizeof(T), cudaMemcpyDeviceToDevice, s));
-        if (p) {
-            CK(cudaStreamSynchronize(s));
-            cudaFree(p);
-        }
+        if (p) cudaFreeAsync(p, alloc_stream());
         p = q;
         cap = nc;
     }
     void exact(uint64_t n) {  // (re)allocate exactly n, contents undefined
         if (n <= cap && n > 0) return;
         release();
-        if (n) CK(cudaMalloc(&p, n * sizeof(T)));
+        if (n) CK(cudaMallocAsync(&p, n * sizeof(T), alloc_stream()));
         cap = n;
     }
 };

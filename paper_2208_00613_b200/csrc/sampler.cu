@@ -901,7 +901,7 @@ struct Tier {
 };
 
 constexpr int kBlkNW = 8;
-constexpr int kBlkU = 4;
+constexpr int kBlkU = IMMX_BLK_U;
 
 template <int KIND>
 uint32_t block_grid(Device& d, const Tier& tier, size_t smem) {
