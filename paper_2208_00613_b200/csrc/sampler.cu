@@ -557,16 +557,18 @@ __device__ __forceinline__ uint32_t advance_row(const uint32_t* cum, uint32_t r,
 // sum of the first `w` entries and of all NW entries of a per-warp smem array
 template <int NW>
 __device__ __forceinline__ void warp_prefix(const uint32_t* a, uint32_t w, uint32_t& before, uint32_t& total) {
-    static_assert(NW % 4 == 0, "NW must be a multiple of 4");
-    before = 0;
-    total = 0;
+    // lanes 0..NW-1 load one entry each and scan with shuffles (called by full warps)
+    static_assert(NW <= 32, "NW must fit a warp");
+    const uint32_t lane = lane_id();
+    uint32_t x = lane < (uint32_t)NW ? a[lane] : 0u;
 #pragma unroll
-    for (int k = 0; k < NW; k += 4) {
-        const uint4 x = *reinterpret_cast<const uint4*>(a + k);
-        before += ((uint32_t)k < w ? x.x : 0u) + ((uint32_t)k + 1 < w ? x.y : 0u) + ((uint32_t)k + 2 < w ? x.z : 0u) +
-                  ((uint32_t)k + 3 < w ? x.w : 0u);
-        total += x.x + x.y + x.z + x.w;
+    for (int o = 1; o < NW; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
     }
+    total = __shfl_sync(0xffffffffu, x, NW - 1);
+    before = __shfl_sync(0xffffffffu, x, (w + NW - 1) % NW);
+    if (w == 0) before = 0;
 }
 
 template <int KIND, int PM, int NW, int U>
@@ -641,13 +643,24 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                 const uint32_t y = __shfl_up_sync(FULL, x, o);
                 if (lane >= (uint32_t)o) x += y;
             }
-            if (lane == 31) sh.wsum[w] = x;
+            // rows without edges are compacted away: every remaining row holds >= 1 edge, so a
+            // window of 32 positions meets at most 33 rows (the mask mapping below needs that)
+            const uint32_t nem = __ballot_sync(FULL, deg > 0);
+            if (lane == 31) {
+                sh.wsum[w] = x;
+                sh.wsum2[w] = __popc(nem);
+            }
             __syncthreads();
-            uint32_t off, total;
+            uint32_t off, total, coff, nrows;
             warp_prefix<NW>(sh.wsum, w, off, total);
-            sh.cum[tid] = x + off;
-            sh.rs[tid] = rs - (uint64_t)(x + off - deg);  // col index of flattened position p = rs + p
-            if (PM == kProbRow) sh.thr[tid] = th;
+            warp_prefix<NW>(sh.wsum2, w, coff, nrows);
+            if (deg > 0) {
+                const uint32_t c = coff + __popc(nem & lt);
+                sh.cum[c] = x + off;
+                sh.rs[c] = rs - (uint64_t)(x + off - deg);  // col index of flattened position p = rs + p
+                if (PM == kProbRow) sh.thr[c] = th;
+            }
+            if (tid >= nrows) sh.cum[tid] = total;
             __syncthreads();
             edges += total;
             qhead += nb;
@@ -679,7 +692,11 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                         else T[i] = Trow;
                     }
                 } else {
-                    // the slice crosses rows: per sub-window, a 5-step search for lanes that need it
+                    // the slice crosses rows.  Per sub-window starting at position a in row r:
+                    // lane j looks at the start of row r+1+j (= cum[r+j]); the OR of the bits
+                    // (start - a - 1) over the warp marks the row starts inside (a, a+32], so
+                    // lane l's row is r + popc(starts at offsets 1..l) and the next sub-window
+                    // starts in row r + popc(all) -- no loop, no search (rows are non-empty).
                     my_multi = a0 < total;
                     uint32_t r = r_w;
 #pragma unroll
@@ -688,19 +705,10 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                         const uint32_t e = a + lane;
                         const bool valid = e < total;
                         const uint32_t ec = min(e, total - 1);
-                        r = advance_row<NW>(sh.cum, r, min(a, total - 1));
-                        uint32_t rr = r;
-                        if (a < total && sh.cum[r] < min(a + 32, total)) {
-                            uint32_t lo = r, hi = min(r + 31, NB - 1);
-#pragma unroll
-                            for (int s = 0; s < 5; ++s) {
-                                const uint32_t mid = (lo + hi) >> 1;
-                                if (sh.cum[mid] > ec) hi = mid;
-                                else lo = mid + 1;
-                            }
-                            rr = lo;
-                        }
-                        r = __shfl_sync(FULL, rr, 31);
+                        const uint32_t rel = sh.cum[min(r + lane, NB - 1)] - a;  // >= 1
+                        const uint32_t M = __reduce_or_sync(FULL, rel - 1 < 32 ? 1u << (rel - 1) : 0u);
+                        const uint32_t rr = min(r + __popc(M & ((1u << lane) - 1u)), NB - 1);
+                        r = min(r + __popc(M), NB - 1);
                         const uint64_t eg = sh.rs[rr] + (uint64_t)ec;
                         v[i] = valid ? __ldg(g.col + eg) : 0u;
                         if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + eg) : 0ull;
