@@ -520,7 +520,8 @@ struct BlkSmem {
     uint64_t thr[NW * 32];   // row threshold (global / per-row modes)
     alignas(16) uint32_t wsum[NW];
     alignas(16) uint32_t wsum2[NW];
-    uint32_t wrow[NW];  // per warp: first row << 16 | last row of its slice of the group
+    uint32_t nextrow[2][NW];  // rows of the next group's warp starts (double-buffered)
+    uint32_t nextpos[2];      // the gpos those rows were computed for
     uint32_t lpos[NW * 32 * U];  // rare path: success positions
     uint32_t lv[NW * 32 * U];    //            and targets
     uint32_t cut;
@@ -666,6 +667,9 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
             qhead += nb;
             uint32_t gpos = 0;
             uint32_t r_w = 0;  // row holding this warp's first position (monotone over the batch)
+            uint32_t par = 0;  // group parity (double buffer of the precomputed start rows)
+            if (tid < 2) sh.nextpos[tid] = 0xffffffffu;
+            __syncthreads();
             while (gpos < total) {
                 // ---- one group: positions gpos + (w*U + i)*32 + lane ----
                 uint32_t v[U];
@@ -675,7 +679,15 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                 uint32_t wd = 0;
                 const uint32_t a0 = gpos + w * U * 32;
                 const uint32_t a0c = min(a0, total - 1);
-                r_w = advance_row<NW>(sh.cum, r_w, a0c);
+                if (sh.nextpos[par] == gpos && a0 < total) r_w = sh.nextrow[par][w];  // precomputed
+                else r_w = advance_row<NW>(sh.cum, r_w, a0c);
+                if (w == 0) {
+                    // the next group's warp starts (valid unless a conflict cut moves gpos):
+                    // NW parallel searches in lanes 0..NW-1, published by this group's barriers
+                    const uint32_t x = gpos + G + lane * U * 32;
+                    if (lane < (uint32_t)NW && x < total) sh.nextrow[par ^ 1][lane] = advance_row<NW>(sh.cum, r_w, x);
+                    if (lane == 0) sh.nextpos[par ^ 1] = gpos + G;
+                }
                 // this warp's slice leaves the row holding gpos -> the group spans several rows
                 bool my_multi = false;
                 if (a0 < total && sh.cum[r_w] >= min(a0 + U * 32, total)) {
@@ -784,6 +796,7 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                     qlen += stotal;
                     t += dtotal;
                     gpos += G;
+                    par ^= 1;
                 } else {
                     // rare: resolve the first position whose target repeats an earlier success
                     {
@@ -866,6 +879,7 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                         }
                     }
                     gpos = cut == 0xffffffffu ? gpos + G : cut;
+                    par ^= 1;
                     __syncthreads();  // rare path: rebuilt visited set, smem success list reuse
                 }
             }
