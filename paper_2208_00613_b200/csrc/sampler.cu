@@ -494,6 +494,11 @@ struct BHash {  // CTA-shared linear-probing hash, load <= 1/2
             i = (i + 1) & (H - 1);
         }
     }
+    __device__ uint32_t find(uint32_t v) const {  // slot of a key that is present
+        uint32_t i = h(v);
+        while (s[i] != v) i = (i + 1) & (H - 1);
+        return i;
+    }
     __device__ void clear_all() {
         const uint4 e = make_uint4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
         for (uint32_t i = threadIdx.x; i < H / 4; i += blockDim.x) reinterpret_cast<uint4*>(s)[i] = e;
@@ -522,6 +527,7 @@ struct BlkSmem {
     alignas(16) uint32_t wsum2[NW];
     uint32_t nextrow[2][NW];  // rows of the next group's warp starts (double-buffered)
     uint32_t nextpos[2];      // the gpos those rows were computed for
+    uint32_t hdup;            // hash tiers: duplicate keys left by conflict rollbacks
     uint32_t lpos[NW * 32 * U];  // rare path: success positions
     uint32_t lv[NW * 32 * U];    //            and targets
     uint32_t cut;
@@ -622,6 +628,7 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
         if (tid == 0) {
             q[0] = root;
             vis.add_test(root);
+            sh.hdup = 0;
         }
         uint32_t qhead = 0, qlen = 1;
         uint64_t edges = 0;
@@ -757,7 +764,7 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                 // the visited set cannot overflow: bitmap tiers hold all n; a hash tier has room
                 // for a whole group.  Otherwise check the capacity first (stotal may count a
                 // repeated target twice -- then the sample just moves to the next tier).
-                const bool early = KIND == kBBits || KIND == kBGlob || qlen + G <= job.qcap;
+                const bool early = KIND == kBBits || KIND == kBGlob || qlen + sh.hdup + G <= job.qcap;
                 bool flag = false;
                 if (early) {
 #pragma unroll
@@ -768,7 +775,7 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
                 uint32_t sbefore, stotal;
                 warp_prefix<NW>(sh.wsum2, w, sbefore, stotal);
                 if (!early) {
-                    if (qlen + stotal > job.qcap) {
+                    if (qlen + sh.hdup + stotal > job.qcap) {
                         overflow = true;
                         break;
                     }
@@ -870,12 +877,34 @@ __global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob 
 #pragma unroll
                             for (int i = 0; i < U; ++i)
                                 if ((sm[i] >> lane) & 1u) vis.add_test(v[i]);
+                        } else if (qlen + sh.hdup + G <= job.qcap) {
+                            // hash: empty the slots of the post-cut successes (located first, then
+                            // cleared: a concurrent probe must not see a half-cleared chain), then
+                            // re-insert the committed successes of this group.  Keys from earlier
+                            // groups never probe through a slot that was empty when they were
+                            // inserted, so their chains stay intact; a committed key may end up
+                            // stored twice -- counted in hdup so the load stays <= 1/2.
+                            uint32_t slot[U];
+#pragma unroll
+                            for (int i = 0; i < U; ++i)
+                                slot[i] = (succ[i] && gpos + (w * U + i) * 32 + lane >= cut) ? vis.find(v[i])
+                                                                                            : 0xffffffffu;
+                            __syncthreads();
+#pragma unroll
+                            for (int i = 0; i < U; ++i)
+                                if (slot[i] != 0xffffffffu) vis.s[slot[i]] = kEmptyKey;
+                            __syncthreads();
+#pragma unroll
+                            for (int i = 0; i < U; ++i)
+                                if ((sm[i] >> lane) & 1u) vis.add_test(v[i]);
+                            if (tid == 0) sh.hdup += s2t;
                         } else {
                             // rebuild the visited set from the committed members
                             __syncthreads();
                             vis.clear_all();
                             __syncthreads();
                             for (uint32_t k = tid; k < qlen; k += blockDim.x) vis.add_test(q[k]);
+                            if (tid == 0) sh.hdup = 0;
                         }
                     }
                     gpos = cut == 0xffffffffu ? gpos + G : cut;
