@@ -247,7 +247,8 @@ IMMX_API int immx_run(const immx_graph* g, const immx_run_config* cfg, immx_resu
 IMMX_API int immx_result_scalars(const immx_result* r, uint64_t* u /*16*/, double* d /*12*/, int* i /*4*/);
 IMMX_API int immx_result_seeds(const immx_result* r, uint32_t* seeds, uint64_t* marginal, double* coverage);
 IMMX_API int immx_result_blocks(const immx_result* r, uint64_t* sets, uint64_t* raw_bytes, uint64_t* encoded_bytes);
-/* device objects the run produced (borrowed; NULL when the mode did not create them) */
+/* device objects the run produced (borrowed; NULL when the mode did not create them).  The
+ * pool is a workspace of the device, reused by the next immx_run on the same device. */
 IMMX_API const immx_pool* immx_result_pool(const immx_result* r);
 IMMX_API const immx_store* immx_result_store(const immx_result* r);
 IMMX_API void immx_result_destroy(immx_result* r);

@@ -170,10 +170,7 @@ struct immx_result {
     std::vector<uint64_t> blk_sets, blk_raw, blk_enc;
     immx_pool* pool = nullptr;
     immx_store* store = nullptr;
-    ~immx_result() {
-        delete pool;
-        delete store;
-    }
+    // pool and store are device workspaces (borrowed), reused by the next run
 };
 
 extern "C" {
@@ -350,6 +347,7 @@ int immx_device_create(int ordinal, immx_device** out) {
         CK(cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, ordinal));
         CK(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
         alloc_stream() = d.stream;
+        if (const char* e = std::getenv("IMMX_SYNC_ALLOC")) async_alloc() = !(e[0] == '1');
         cudaMemPool_t mp;
         CK(cudaDeviceGetDefaultMemPool(&mp, ordinal));
         uint64_t keep_all = ~0ULL;  // keep freed memory in the pool for the next run
@@ -363,6 +361,10 @@ void immx_device_destroy(immx_device* h) {
     if (!h) return;
     cudaStreamSynchronize(h->d.stream);
     if (h->d.host_scal) cudaFreeHost(h->d.host_scal);
+    delete h->d.run_pool;
+    h->d.run_pool = nullptr;
+    delete h->d.run_store;
+    h->d.run_store = nullptr;
     h->d.scal.release();
     h->d.tmp.release();
     if (alloc_stream() == h->d.stream) alloc_stream() = nullptr;  // objects outliving it free on stream 0
@@ -805,9 +807,15 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
 
         auto* R = new immx_result;
         std::unique_ptr<immx_result> guard_r(R);
-        R->pool = new immx_pool;
+        // the device keeps the run's pool (its multi-GB arena) for the next run; the result
+        // borrows it (valid until the next immx_run on this device)
+        if (!d.run_pool) {
+            d.run_pool = new immx_pool;
+            d.run_pool->p.dev = &d;
+        }
+        R->pool = d.run_pool;
         Pool& pool = R->pool->p;
-        pool.dev = &d;
+        pool.count = pool.members = pool.edges = pool.arena_used = 0;
 
         // ---- theta estimation (pipeline.cpp:61-63) ----
         auto t0 = Clock::now();
@@ -837,7 +845,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         int mode = IMMX_MODE_RAW, char_mode = IMMX_MODE_RAW;
         double skew = 0.0, dens = 0.0;
         HostCodebook cb;
-        std::unique_ptr<immx_store> store;
+        immx_store* store = nullptr;  // the device's run store (borrowed by the result)
         std::unique_ptr<immx_bitmap> bm;
         DBuf<unsigned int> hist;  // encoding-time table (huffman)
         hist.exact(std::max<uint64_t>(n, 1));
@@ -875,7 +883,9 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     std::vector<unsigned long long> lut;
                     uint32_t rb = 1;
                     build_decode_lut(cb, lut, rb);
-                    store.reset(new immx_store);
+                    if (!d.run_store) d.run_store = new immx_store;
+                    store = d.run_store;
+                    store->s.count = store->s.total_words = store->s.total_copied = store->s.payload_bytes = 0;
                     store_set_codes(store->s, d, n, cb.bits.data(), cb.len.data(), lut, rb);
                 } else if (mode == IMMX_MODE_BITMAP) {
                     bm.reset(new immx_bitmap);
@@ -990,7 +1000,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         R->seeds = sel.seeds;
         R->marginal = sel.marginal;
         R->coverage = sel.coverage;
-        R->store = store.release();
+        R->store = store;
         *out = guard_r.release();
     });
 }

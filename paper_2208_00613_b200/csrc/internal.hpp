@@ -10,6 +10,9 @@
 #include "immx_b200.h"
 #include "common.cuh"
 
+struct immx_pool;
+struct immx_store;
+
 namespace immx_dev {
 
 // Exceptions carry the C-ABI status they map to (reference error classes, SURVEY §5:
@@ -33,6 +36,20 @@ inline cudaStream_t& alloc_stream() {
     static cudaStream_t s = nullptr;
     return s;
 }
+inline bool& async_alloc() {  // IMMX_SYNC_ALLOC=1 selects plain cudaMalloc/cudaFree
+    static bool a = true;
+    return a;
+}
+inline cudaError_t dmalloc(void** p, size_t bytes) {
+    return async_alloc() ? cudaMallocAsync(p, bytes, alloc_stream()) : cudaMalloc(p, bytes);
+}
+inline void dfree(void* p) {
+    if (async_alloc()) cudaFreeAsync(p, alloc_stream());
+    else {
+        cudaStreamSynchronize(alloc_stream());
+        cudaFree(p);
+    }
+}
 
 // A growable device buffer (never shrinks; contents preserved on growth).
 template <class T>
@@ -41,7 +58,7 @@ struct DBuf {
     uint64_t cap = 0;
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFreeAsync(p, alloc_stream());
+        if (p) dfree(p);
         p = nullptr;
         cap = 0;
     }
@@ -50,16 +67,16 @@ struct DBuf {
         uint64_t nc = cap ? cap : 1024;
         while (nc < n) nc += nc / 2 + 1024;
         T* q = nullptr;
-        CK(cudaMallocAsync(&q, nc * sizeof(T), alloc_stream()));
+        CK(dmalloc(reinterpret_cast<void**>(&q), nc * sizeof(T)));
         if (keep && p && cap) CK(cudaMemcpyAsync(q, p, cap * sizeof(T), cudaMemcpyDeviceToDevice, s));
-        if (p) cudaFreeAsync(p, alloc_stream());
+        if (p) dfree(p);
         p = q;
         cap = nc;
     }
     void exact(uint64_t n) {  // (re)allocate exactly n, contents undefined
         if (n <= cap && n > 0) return;
         release();
-        if (n) CK(cudaMallocAsync(&p, n * sizeof(T), alloc_stream()));
+        if (n) CK(dmalloc(reinterpret_cast<void**>(&p), n * sizeof(T)));
         cap = n;
     }
 };
@@ -92,6 +109,18 @@ struct Device {
     DBuf<unsigned long long> scal;  // general device scalars
     DBuf<uint8_t> tmp;              // CUB temp storage
     void* host_scal = nullptr;      // pinned host mirror of scal (64 x u64)
+    // grow-only workspaces reused across calls (a run allocates them once; later runs and
+    // later estimation iterations reuse them, so the allocator never churns on GB buffers)
+    DBuf<uint32_t> ws_list[2], ws_nospace, ws_qscratch, ws_gbits;
+    DBuf<unsigned long long> ws_ctl;
+    DBuf<unsigned int> ws_hist;
+    DBuf<uint64_t> ws_idx_off, ws_cnt64;
+    DBuf<unsigned long long> ws_cursor;
+    DBuf<uint32_t> ws_idx;
+    DBuf<uint8_t> ws_covered, ws_is_seed;
+    // the RRR pool of immx_run (reused by the next run on this device)
+    struct ::immx_pool* run_pool = nullptr;
+    struct ::immx_store* run_store = nullptr;  // likewise the run's Huffman store
 };
 
 struct DevGraph {

@@ -203,17 +203,18 @@ void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
     const uint64_t theta = P.count;
     if (theta == 0) fail(IMMX_EINVAL, "selection requires at least one set");
     if (k >= n) fail(IMMX_EINVAL, "selection requires k < n");
-    DBuf<unsigned int> hist;
+    // device workspaces (grow-only, reused by every estimation iteration and run)
+    DBuf<unsigned int>& hist = d.ws_hist;
     hist.exact(n);
     CK(cudaMemsetAsync(hist.p, 0, n * 4, s));
     pool_hist_dev(P, 0, theta, hist.p);
     // inverted index: idx_off = exclusive scan of counts (u64)
-    DBuf<uint64_t> idx_off;
+    DBuf<uint64_t>& idx_off = d.ws_idx_off;
     idx_off.exact(n + 1);
-    DBuf<unsigned long long> cursor;
+    DBuf<unsigned long long>& cursor = d.ws_cursor;
     cursor.exact(n + 1);
     {
-        DBuf<uint64_t> cnt64;
+        DBuf<uint64_t>& cnt64 = d.ws_cnt64;
         cnt64.exact(n + 1);
         CK(cudaMemsetAsync(cnt64.p, 0, (n + 1) * 8, s));
         u32_to_u64_dev(d, hist.p, n, cnt64.p + 1);
@@ -224,12 +225,13 @@ void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
         CK(cudaMemcpyAsync(cursor.p, idx_off.p, (n + 1) * 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaStreamSynchronize(s));
     }
-    DBuf<uint32_t> idx;
-    idx.exact(std::max<uint64_t>(P.members, 1));
+    DBuf<uint32_t>& idx = d.ws_idx;
+    if (idx.cap < P.members) idx.exact(P.members + P.members / 2 + 1024);  // grows geometrically
     k_index_fill<<<grid_for(theta * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, theta, cursor.p, idx.p);
     CK_LAUNCH("k_index_fill");
     d.kernel_launches++;
-    DBuf<uint8_t> covered, is_seed;
+    DBuf<uint8_t>& covered = d.ws_covered;
+    DBuf<uint8_t>& is_seed = d.ws_is_seed;
     covered.exact(theta);
     is_seed.exact(n);
     CK(cudaMemsetAsync(covered.p, 0, theta, s));

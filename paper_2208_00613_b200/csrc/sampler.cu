@@ -1083,12 +1083,14 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         tiers.push_back({kVisGlobBits, 0, 4, (uint32_t)std::min<uint64_t>(G.n, 0xffffffffu)});
     }
 
-    DBuf<uint32_t> lists[2];
-    DBuf<uint32_t> nospace;
-    DBuf<uint32_t> qscratch;
-    DBuf<uint32_t> gbits;
-    DBuf<SampCtl> ctl;
-    ctl.exact(1);
+    DBuf<uint32_t>* lists = d.ws_list;  // device workspaces, reused across calls
+    DBuf<uint32_t>& nospace = d.ws_nospace;
+    DBuf<uint32_t>& qscratch = d.ws_qscratch;
+    DBuf<uint32_t>& gbits = d.ws_gbits;
+    d.ws_ctl.exact((sizeof(SampCtl) + 7) / 8);
+    struct {
+        SampCtl* p;
+    } ctl{reinterpret_cast<SampCtl*>(d.ws_ctl.p)};
     SampCtl* hctl = static_cast<SampCtl*>(d.host_scal);
     lists[0].exact(count);
     lists[1].exact(count);
