@@ -135,6 +135,13 @@ IMMX_API int immx_device_reset_stats(immx_device* d);
  * (weighted cascade, uniform) are stored per row / once. */
 IMMX_API int immx_graph_upload(immx_device* d, uint64_t n, uint64_t m, const uint64_t* offsets,
                       const uint32_t* targets, const double* probs, int transposed, immx_graph** out);
+/* Synthetic R-MAT generated directly in HBM as the reverse CSR -- the same graph as
+ * immx_hgraph_generate_rmat + transpose (bit-identical), without host memory or a transpose.
+ * weight_model 0 = weighted cascade fl32(1/indeg(v)), 1 = uniform fl32(p). */
+IMMX_API int immx_graph_generate_rmat(immx_device* d, uint32_t scale, uint32_t edge_factor, double a, double b,
+                                      double c, uint64_t seed, int weight_model, double p, immx_graph** out);
+/* D2H of the reverse CSR (row[n+1], col[m]) and f64 probabilities per Gt edge (prob may be NULL) */
+IMMX_API int immx_graph_download(const immx_graph* g, uint64_t* row, uint32_t* col, double* prob);
 /* LT extension: per-Gt-edge weights (Gt CSR order). */
 IMMX_API int immx_graph_set_lt_weights(immx_graph* g, const float* weights);
 IMMX_API int immx_graph_info(const immx_graph* g, uint64_t* n, uint64_t* m, int* prob_mode);

@@ -245,6 +245,29 @@ class DeviceGraph:
         self.h = h
         return self
 
+    @classmethod
+    def generate_rmat(cls, scale, edge_factor, a=0.57, b=0.19, c=0.19, seed=1, weights="wc", p=0.1, device=None):
+        """R-MAT generated in HBM as the reverse CSR (identical to generate_rmat + transpose)."""
+        self = cls.__new__(cls)
+        self.device = device or default_device()
+        h = C.c_void_p()
+        check(lib.immx_graph_generate_rmat(self.device.h, scale, edge_factor, a, b, c, seed, _weight_model(weights), p,
+                                           C.byref(h)))
+        self.h = h
+        n, m = C.c_uint64(), C.c_uint64()
+        check(lib.immx_graph_info(h, C.byref(n), C.byref(m), None))
+        self.n, self.m = n.value, m.value
+        return self
+
+    def download(self, probs: bool = True):
+        """-> (row u64[n+1], col u32[m], prob f64[m] or None): the reverse CSR."""
+        row = np.zeros(self.n + 1, np.uint64)
+        col = np.zeros(max(self.m, 1), np.uint32)
+        pr = np.zeros(max(self.m, 1), np.float64) if probs else None
+        check(lib.immx_graph_download(self.h, ptr(row, C.c_uint64), ptr(col, C.c_uint32),
+                                      None if pr is None else ptr(pr, C.c_double)))
+        return row, col[: self.m], None if pr is None else pr[: self.m]
+
     @property
     def prob_mode(self) -> str:
         pm = C.c_int()

@@ -421,6 +421,30 @@ int immx_graph_upload(immx_device* dv, uint64_t n, uint64_t m, const uint64_t* o
         *out = g;
     });
 }
+int immx_graph_generate_rmat(immx_device* dv, uint32_t scale, uint32_t ef, double a, double b, double c,
+                             uint64_t seed, int weight_model, double p, immx_graph** out) {
+    return guard([&] {
+        need(dv, "device");
+        need(out, "out");
+        if (weight_model != 0 && weight_model != 1) fail(IMMX_EINVAL, "unknown weight model");
+        auto* g = new immx_graph;
+        try {
+            graph_generate_rmat(g->g, dv->d, scale, ef, a, b, c, seed, weight_model, p);
+        } catch (...) {
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+int immx_graph_download(const immx_graph* g, uint64_t* row, uint32_t* col, double* prob) {
+    return guard([&] {
+        need(g, "graph");
+        need(row, "row");
+        if (g->g.m) need(col, "col");
+        graph_download(g->g, row, col, prob);
+    });
+}
 int immx_graph_set_lt_weights(immx_graph* g, const float* w) {
     return guard([&] {
         need(g, "graph");

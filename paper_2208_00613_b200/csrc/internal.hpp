@@ -185,6 +185,10 @@ struct SelectOut {
 void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt,
                   const double* prob, bool transposed);
 void graph_set_lt(DevGraph& G, const float* w);
+// device_gen.cu
+void graph_generate_rmat(DevGraph& G, Device& d, uint32_t scale, uint32_t ef, double a, double b, double c,
+                         uint64_t seed, int weight_model, double p);
+void graph_download(const DevGraph& G, uint64_t* row, uint32_t* col, double* prob);
 // sampler.cu
 void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first, uint64_t seed,
                       const uint32_t* d_roots, const uint64_t* d_states, int model);

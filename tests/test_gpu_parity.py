@@ -306,3 +306,39 @@ def test_lt_walk(im, orc):
     pool.sample(dg, 2000, 0, 42, model=1)
     off, mem = pool.read()
     assert_same_sets(a[0], a[1], off, mem)
+
+
+# ------------------------------------------------------------------ device generator
+@pytest.mark.parametrize("weights,p", [("wc", 0.0), ("uniform", 0.01)])
+def test_device_rmat_equals_host(im, orc, weights, p):
+    # the in-HBM generator emits exactly transpose(host generator) with the same weights
+    for scale, ef, seed in ((10, 8, 3), (14, 16, 1)):
+        h = im.generate_rmat(scale, ef, 0.57, 0.19, 0.19, seed)
+        im.assign_weights_f32(h, weights, p)
+        ht = csr_of(im.transpose(h))
+        dg = im.DeviceGraph.generate_rmat(scale, ef, 0.57, 0.19, 0.19, seed, weights=weights, p=p)
+        row, col, pr = dg.download()
+        assert np.array_equal(row, ht.off) and np.array_equal(col, ht.tgt) and np.array_equal(pr, ht.prob)
+        pool = im.Pool(dg.device)
+        pool.sample(dg, 500, 0, 42)
+        off, mem = pool.read()
+        a = orc.sample_block(ht, 500, 0, 42)
+        assert_same_sets(a[0], a[1], off, mem)
+
+
+def test_device_rmat_c2_matches_golden_graph(im):
+    import hashlib
+    import json
+    import os
+    from conftest import GOLDEN
+
+    g = json.load(open(os.path.join(GOLDEN, "golden.json")))["cases"]["c2"]
+    dg = im.DeviceGraph.generate_rmat(18, 16, 0.57, 0.19, 0.19, 1, weights="uniform", p=0.01)
+    for w in g["windows"]:
+        pool = im.Pool(dg.device)
+        pool.sample(dg, w["count"], w["first"], 42)
+        off, mem = pool.read()
+        h = hashlib.sha256()
+        h.update(np.ascontiguousarray(off).tobytes())
+        h.update(np.ascontiguousarray(mem).tobytes())
+        assert h.hexdigest() == w["sha"]
