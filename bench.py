@@ -37,7 +37,10 @@ CONFIGS = {
     "c2": dict(gen=("rmat", 18, 16, 1), weights=("uniform", 0.01), k=50, eps=0.5, blocks=8, mode="huffman",
                desc="R-MAT scale 18 EF16 (.57,.19,.19) seed 1, IC p=fl32(0.01), k=50 eps=0.5 b=8 huffman"),
     "c4": dict(gen=("rmat", 22, 24, 3), weights=("wc", 0.0), k=100, eps=0.13, blocks=8, mode="huffman",
-               desc="R-MAT scale 22 EF24 seed 3, WC fl32, k=100 eps=0.13 b=8 huffman"),
+               desc="R-MAT scale 22 EF24 seed 3, WC fl32, k=100 eps=0.13 b=8 huffman", device_gen=True),
+    "c5": dict(gen=("rmat", 25, 42, 4), weights=("wc", 0.0), k=50, eps=0.5, blocks=8, mode="huffman",
+               desc="R-MAT scale 25 EF42 seed 4, WC fl32, k=50 eps=0.5 b=8 huffman (hybrid degenerates: no set > n/32)",
+               device_gen=True),
 }
 METRIC = "RRR samples/s & achieved HBM GB/s at 1 B200; IMM end-to-end s; compress ratio"
 SEED = 42
@@ -145,7 +148,7 @@ def barrier(world):
 
 
 # ------------------------------------------------------------------ CPU arms
-def cpu_reference_rate(g_arrays, n, samples: int, first: int, threads: int):
+def cpu_reference_rate(g_arrays, n, samples: int, first: int, threads: int, transposed: bool = False):
     """The unmodified reference (oracle/_ref, compiled from its sources) sampling
     `samples` RRR sets of the workload with `threads` OpenMP workers -> (samples/s, seconds)."""
     from oracle.oracle import CSR, RefLib
@@ -153,7 +156,7 @@ def cpu_reference_rate(g_arrays, n, samples: int, first: int, threads: int):
     off, tgt, pr = g_arrays
     ref = RefLib()
     rg = ref.graph(CSR(n, off, tgt, pr))
-    rgt = rg.transpose()
+    rgt = rg if transposed else rg.transpose()
     t0 = time.perf_counter()
     rgt.sample_block(samples, first, SEED, threads)
     dt = time.perf_counter() - t0
@@ -216,10 +219,19 @@ def run_ours(args, cfg, rank, world, local):
     torch.cuda.set_device(local)
     dev = im.Device(local)
     stream = torch.cuda.ExternalStream(dev.stream, device=f"cuda:{local}")
-    g = make_graph(im, cfg)
-    off, tgt, pr, _ = g.arrays()
+    transposed = bool(cfg.get("device_gen"))
+    if transposed:
+        # large configs: generated in HBM as the reverse CSR (identical to the host generator +
+        # transpose, tests/test_gpu_parity.py); the e2e leg uploads that reverse CSR from host
+        gen = cfg["gen"]
+        dg = im.DeviceGraph.generate_rmat(gen[1], gen[2], 0.57, 0.19, 0.19, gen[3], weights=cfg["weights"][0],
+                                          p=cfg["weights"][1], device=dev)
+        off, tgt, pr = dg.download()
+    else:
+        g = make_graph(im, cfg)
+        off, tgt, pr, _ = g.arrays()
+        dg = im.DeviceGraph.from_arrays(int(off.size - 1), off, tgt, pr, False, device=dev)
     n, m = int(off.size - 1), int(tgt.size)
-    dg = im.DeviceGraph.from_arrays(n, off, tgt, pr, False, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")  # > L2 (126 MB)
     run_kw = dict(epsilon=cfg["eps"], blocks=cfg["blocks"], mode=cfg["mode"], seed=SEED)
 
@@ -277,7 +289,7 @@ def run_ours(args, cfg, rank, world, local):
     e2e_samples = 0
     e2e_steps = max(1, min(args.steps, 3))
     for _ in range(e2e_steps):
-        dge = im.DeviceGraph.from_arrays(n, p_off, p_tgt, p_pr, False, device=dev)
+        dge = im.DeviceGraph.from_arrays(n, p_off, p_tgt, p_pr, transposed, device=dev)
         r = im.run_device(dge, cfg["k"], **run_kw)  # results land in host memory
         e2e_samples += r["samples_drawn"]
         del dge
@@ -306,7 +318,7 @@ def run_ours(args, cfg, rank, world, local):
     if world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            rate, dt = cpu_reference_rate((off, tgt, pr), n, args.ref_samples, 0, threads)
+            rate, dt = cpu_reference_rate((off, tgt, pr), n, args.ref_samples, 0, threads, transposed)
             cpu = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "reference",
                    "sample": f"reference sample_block, global indices [0, {args.ref_samples}) of the workload, "
                              f"{dt:.1f} s on {threads} host threads"}
