@@ -36,6 +36,9 @@ CONFIGS = {
                desc="ER n=10k m=100k seed 0, WC fl32, k=10 eps=0.5 b=10 huffman"),
     "c2": dict(gen=("rmat", 18, 16, 1), weights=("uniform", 0.01), k=50, eps=0.5, blocks=8, mode="huffman",
                desc="R-MAT scale 18 EF16 (.57,.19,.19) seed 1, IC p=fl32(0.01), k=50 eps=0.5 b=8 huffman"),
+    "c3": dict(gen=("rmat", 20, 16, 2), weights=("wc", 0.0), k=100, eps=0.5, blocks=8, mode="huffman",
+               desc="R-MAT scale 20 EF16 seed 2, LT (in-weights U(0,1) normalised, f32, seed 3), k=100 eps=0.5 b=8 "
+                    "(hybrid degenerates to huffman: no set > n/32)", device_gen=True, lt_seed=3),
     "c4": dict(gen=("rmat", 22, 24, 3), weights=("wc", 0.0), k=100, eps=0.13, blocks=8, mode="huffman",
                desc="R-MAT scale 22 EF24 seed 3, WC fl32, k=100 eps=0.13 b=8 huffman", device_gen=True),
     "c5": dict(gen=("rmat", 25, 42, 4), weights=("wc", 0.0), k=50, eps=0.5, blocks=8, mode="huffman",
@@ -234,6 +237,9 @@ def run_ours(args, cfg, rank, world, local):
     n, m = int(off.size - 1), int(tgt.size)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")  # > L2 (126 MB)
     run_kw = dict(epsilon=cfg["eps"], blocks=cfg["blocks"], mode=cfg["mode"], seed=SEED)
+    if "lt_seed" in cfg:  # config 3: LT diffusion (extension; weights generated in HBM)
+        dg.set_lt_random(cfg["lt_seed"])
+        run_kw["model"] = 1
 
     def one_step():
         return im.run_device(dg, cfg["k"], **run_kw)
@@ -290,6 +296,8 @@ def run_ours(args, cfg, rank, world, local):
     e2e_steps = max(1, min(args.steps, 3))
     for _ in range(e2e_steps):
         dge = im.DeviceGraph.from_arrays(n, p_off, p_tgt, p_pr, transposed, device=dev)
+        if "lt_seed" in cfg:
+            dge.set_lt_random(cfg["lt_seed"])
         r = im.run_device(dge, cfg["k"], **run_kw)  # results land in host memory
         e2e_samples += r["samples_drawn"]
         del dge

@@ -144,6 +144,8 @@ IMMX_API int immx_graph_generate_rmat(immx_device* d, uint32_t scale, uint32_t e
 IMMX_API int immx_graph_download(const immx_graph* g, uint64_t* row, uint32_t* col, double* prob);
 /* LT extension: per-Gt-edge weights (Gt CSR order). */
 IMMX_API int immx_graph_set_lt_weights(immx_graph* g, const float* weights);
+/* LT extension: the generator's weights (immx_hgraph_lt_weights on Gt) computed in place. */
+IMMX_API int immx_graph_set_lt_random(immx_graph* g, uint64_t seed);
 IMMX_API int immx_graph_info(const immx_graph* g, uint64_t* n, uint64_t* m, int* prob_mode);
 IMMX_API void immx_graph_destroy(immx_graph* g);
 

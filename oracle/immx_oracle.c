@@ -188,6 +188,17 @@ OC_API oc_block* oc_sample_block(uint64_t n, const uint64_t* off, const uint32_t
     return b;
 }
 
+/* LT extension (self-pinned, see oc_sample_lt): while an oc_*_lt entry point runs, the
+ * estimation and production sampling use the reverse random walk with these Gt weights. */
+static const float* oc_lt_w = NULL;
+OC_API oc_block* oc_sample_block_lt(uint64_t n, const uint64_t* off, const uint32_t* tgt, const float* w,
+                                    uint64_t count, uint64_t first, uint64_t seed);
+static oc_block* oc_sample_any(uint64_t n, const uint64_t* off, const uint32_t* tgt, const double* prob,
+                               uint64_t count, uint64_t first, uint64_t seed) {
+    if (oc_lt_w) return oc_sample_block_lt(n, off, tgt, oc_lt_w, count, first, seed);
+    return oc_sample_block(n, off, tgt, prob, count, first, seed);
+}
+
 /* Python-facing sample_rrr(g_t, root, seed): raw Rng(seed), no stream_for
  * (proj/bindings/module.cpp:110-116). Returns size or -1 if cap exceeded. */
 OC_API int64_t oc_sample_rrr_seed(uint64_t n, const uint64_t* off, const uint32_t* tgt,
@@ -310,7 +321,7 @@ OC_API void oc_estimate_theta(uint64_t n, const uint64_t* off, const uint32_t* t
     for (uint32_t i = 1; i <= i_max; ++i) {
         const uint64_t theta_i = (uint64_t)ceil(base * exp2((double)i));
         if (theta_i > sampled) {
-            oc_block* b = oc_sample_block(n, off, tgt, prob, theta_i - sampled, sampled, seed);
+            oc_block* b = oc_sample_any(n, off, tgt, prob, theta_i - sampled, sampled, seed);
             if (theta_i + 1 > off_cap) {
                 off_cap = theta_i + 1;
                 set_off = (uint64_t*)realloc(set_off, sizeof(uint64_t) * off_cap);
@@ -854,7 +865,7 @@ OC_API oc_run_result* oc_run(uint64_t n, uint64_t m, const uint64_t* off, const 
     uint64_t* bm_wpr = (uint64_t*)calloc(b, sizeof(uint64_t));
     for (uint32_t i = 1; i <= b; ++i) {
         const uint64_t count = per_block < theta - done ? per_block : theta - done;
-        oc_block* blk = oc_sample_block(n, t_off, t_tgt, t_prob, count, done, seed);
+        oc_block* blk = oc_sample_any(n, t_off, t_tgt, t_prob, count, done, seed);
         if (total + blk->total > mcap) {
             mcap = (total + blk->total) * 2 + 16;
             R->members = (uint32_t*)realloc(R->members, sizeof(uint32_t) * mcap);
@@ -1140,4 +1151,23 @@ OC_API oc_block* oc_sample_block_lt(uint64_t n, const uint64_t* off, const uint3
     }
     free(mark);
     return b;
+}
+
+/* LT pipeline entry points: estimate_theta / run with LT walks (weights per Gt edge, in the
+ * order oc_transpose produces). Same control flow as the IC ones. */
+OC_API void oc_estimate_theta_lt(uint64_t n, const uint64_t* off, const uint32_t* tgt, const float* w, uint32_t k,
+                                 double eps, uint64_t seed, uint64_t* out, double* covered_fraction) {
+    double* dummy = (double*)calloc(off[n] ? off[n] : 1, sizeof(double));
+    oc_lt_w = w;
+    oc_estimate_theta(n, off, tgt, dummy, k, eps, seed, out, covered_fraction);
+    oc_lt_w = NULL;
+    free(dummy);
+}
+OC_API oc_run_result* oc_run_lt(uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt, const double* prob,
+                                const float* w_t, uint32_t k, double eps, uint32_t blocks, int mode_override,
+                                uint64_t seed, int workers) {
+    oc_lt_w = w_t;
+    oc_run_result* R = oc_run(n, m, off, tgt, prob, k, eps, blocks, mode_override, seed, workers);
+    oc_lt_w = NULL;
+    return R;
 }

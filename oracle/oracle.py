@@ -98,6 +98,10 @@ class Oracle:
              [u32p, u64p, u64p, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint32, u32p, u64p, f64p])
         _sig(L, "oc_run", P, [C.c_uint64, C.c_uint64, u64p, u32p, f64p, C.c_uint32, C.c_double,
                               C.c_uint32, C.c_int, C.c_uint64, C.c_int])
+        _sig(L, "oc_run_lt", P, [C.c_uint64, C.c_uint64, u64p, u32p, f64p, f32p, C.c_uint32, C.c_double,
+                                 C.c_uint32, C.c_int, C.c_uint64, C.c_int])
+        _sig(L, "oc_estimate_theta_lt", None,
+             [C.c_uint64, u64p, u32p, f32p, C.c_uint32, C.c_double, C.c_uint64, u64p, C.POINTER(C.c_double)])
         _sig(L, "oc_run_scalars", None, [P, u64p, f64p, i32p])
         _sig(L, "oc_run_seeds", None, [P, u32p, u64p, f64p])
         _sig(L, "oc_run_blocks", None, [P, u64p, u64p, u64p, u32p])
@@ -246,10 +250,15 @@ class Oracle:
 
     # ------------------------------------------------------------- pipeline
     def run(self, g: CSR, k: int, epsilon: float = 0.5, blocks: int = 8, mode: str = "auto",
-            seed: int = 42, workers: int = 1, want_store: bool = False, want_pool: bool = False):
+            seed: int = 42, workers: int = 1, want_store: bool = False, want_pool: bool = False, lt_weights=None):
         """pipeline.cpp:47-178 on the FORWARD graph g."""
         m = -1 if mode == "auto" else MODES[mode]
-        h = self.L.oc_run(g.n, g.m, g.off, _nz32(g.tgt), _nz64(g.prob), k, epsilon, blocks, m, seed, workers)
+        if lt_weights is not None:  # LT extension: weights per Gt edge (oc_transpose order)
+            w = np.ascontiguousarray(lt_weights, np.float32)
+            h = self.L.oc_run_lt(g.n, g.m, g.off, _nz32(g.tgt), _nz64(g.prob), w if w.size else np.zeros(1, np.float32),
+                                 k, epsilon, blocks, m, seed, workers)
+        else:
+            h = self.L.oc_run(g.n, g.m, g.off, _nz32(g.tgt), _nz64(g.prob), k, epsilon, blocks, m, seed, workers)
         u = np.zeros(13, np.uint64)
         d = np.zeros(5, np.float64)
         i = np.zeros(3, np.int32)

@@ -268,6 +268,15 @@ class DeviceGraph:
                                       None if pr is None else ptr(pr, C.c_double)))
         return row, col[: self.m], None if pr is None else pr[: self.m]
 
+    def set_lt_weights(self, weights):
+        """LT extension: per-Gt-edge float32 weights (Gt CSR order)."""
+        w = arr(weights, np.float32)
+        check(lib.immx_graph_set_lt_weights(self.h, ptr(w, C.c_float)))
+
+    def set_lt_random(self, seed: int):
+        """LT extension: the generator's U(0,1)-normalised weights, computed in HBM."""
+        check(lib.immx_graph_set_lt_random(self.h, seed))
+
     @property
     def prob_mode(self) -> str:
         pm = C.c_int()
@@ -733,9 +742,11 @@ def run_device(dg: DeviceGraph, k: int, *, epsilon=0.5, blocks=8, mode="auto", s
 
 
 def run(graph: Graph, k: int, *, epsilon=0.5, blocks=8, mode="auto", seed=42, workers=1, merged_argmax=False,
-        reuse_pool=True):
+        reuse_pool=True, diffusion="ic", lt_seed=0, lt_weights=None):
     """The IMM driver (pipeline.cpp:47-178) -> {seeds, marginal, coverage, padded, seed_ids, stats}.
-    The graph (forward) is uploaded and transposed on the device."""
+    The graph (forward) is uploaded and transposed on the device.  diffusion="lt" (extension,
+    no reference counterpart) samples reverse LT walks with `lt_weights` (per Gt edge) or the
+    generator's weights for `lt_seed`."""
     n = graph.n
     if k < 1 or k >= n:
         raise ValueError("k must satisfy 1 <= k < n")
@@ -745,9 +756,18 @@ def run(graph: Graph, k: int, *, epsilon=0.5, blocks=8, mode="auto", seed=42, wo
         raise ValueError("block count must be >= 2")
     if mode != "auto" and mode not in _MODE_ID:
         raise ValueError(f"unknown mode '{mode}'")
+    if diffusion not in ("ic", "lt"):
+        raise ValueError(f"unknown diffusion model '{diffusion}'")
     dg = DeviceGraph(graph, transposed=False)
+    model = _capi.MODEL_IC
+    if diffusion == "lt":
+        model = _capi.MODEL_LT
+        if lt_weights is not None:
+            dg.set_lt_weights(lt_weights)
+        else:
+            dg.set_lt_random(lt_seed)
     r = run_device(dg, k, epsilon=epsilon, blocks=blocks, mode=mode, seed=seed, workers=workers,
-                   reuse_pool=reuse_pool)
+                   reuse_pool=reuse_pool, model=model)
     ids = graph.original_ids
     theta = r["theta"]
     stats = {

@@ -87,6 +87,7 @@ SIGNATURES = {
     "immx_graph_generate_rmat": (I, [P, u32, u32, dbl, dbl, dbl, u64, I, dbl, PP]),
     "immx_graph_download": (I, [P, pu64, pu32, pdbl]),
     "immx_graph_set_lt_weights": (I, [P, pflt]),
+    "immx_graph_set_lt_random": (I, [P, u64]),
     "immx_graph_info": (I, [P, pu64, pu64, pint]),
     "immx_graph_destroy": (None, [P]),
     "immx_pool_create": (I, [P, PP]),

@@ -445,6 +445,12 @@ int immx_graph_download(const immx_graph* g, uint64_t* row, uint32_t* col, doubl
         graph_download(g->g, row, col, prob);
     });
 }
+int immx_graph_set_lt_random(immx_graph* g, uint64_t seed) {
+    return guard([&] {
+        need(g, "graph");
+        graph_set_lt_random(g->g, seed);
+    });
+}
 int immx_graph_set_lt_weights(immx_graph* g, const float* w) {
     return guard([&] {
         need(g, "graph");

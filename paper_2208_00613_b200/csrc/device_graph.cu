@@ -110,6 +110,27 @@ __global__ void k_lt_cum(const uint64_t* __restrict__ row, const float* __restri
     }
 }
 
+// LT weights generated in place (graph_host.cpp lt_weights + k_lt_cum in one pass): Gt edge e
+// of row v draws U(0,1) from stream (seed ^ 0x4c54, e); the row is normalised by its sequential
+// double sum, rounded to float32, and the running double sums are kept.
+__global__ void k_lt_random_cum(const uint64_t* __restrict__ row, uint64_t n, uint64_t seed, double* __restrict__ cum) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = row[v], e = row[v + 1];
+        double sum = 0.0;
+        for (uint64_t i = b; i < e; ++i) {
+            const uint64_t s = stream_state(seed ^ 0x4c54ULL, i) + kGamma;
+            sum += (double)(mix64(s) >> 11) * 0x1.0p-53;
+        }
+        double acc = 0.0;
+        for (uint64_t i = b; i < e; ++i) {
+            const uint64_t s = stream_state(seed ^ 0x4c54ULL, i) + kGamma;
+            const double raw = (double)(mix64(s) >> 11) * 0x1.0p-53;
+            acc += (double)(float)(sum > 0 ? __ddiv_rn(raw, sum) : 0.0);
+            cum[i] = acc;
+        }
+    }
+}
+
 unsigned grid_for(uint64_t items, const Device& d, unsigned per_thread = 1) {
     uint64_t b = (items / per_thread + 255) / 256;
     b = std::min<uint64_t>(b, (uint64_t)d.num_sms * 16);
@@ -229,6 +250,17 @@ void graph_set_lt(DevGraph& G, const float* w) {
     if (G.m) CK(cudaMemcpyAsync(dw.p, w, G.m * 4, cudaMemcpyHostToDevice, s));
     G.lt_cum.exact(std::max<uint64_t>(G.m, 1));
     k_lt_cum<<<grid_for(G.n, d), 256, 0, s>>>(G.row.p, dw.p, G.n, G.lt_cum.p);
+    d.kernel_launches++;
+    CK(cudaStreamSynchronize(s));
+    G.has_lt = true;
+}
+
+void graph_set_lt_random(DevGraph& G, uint64_t seed) {
+    Device& d = *G.dev;
+    cudaStream_t s = d.stream;
+    G.lt_cum.exact(std::max<uint64_t>(G.m, 1));
+    k_lt_random_cum<<<grid_for(G.n, d), 256, 0, s>>>(G.row.p, G.n, seed, G.lt_cum.p);
+    CK_LAUNCH("k_lt_random_cum");
     d.kernel_launches++;
     CK(cudaStreamSynchronize(s));
     G.has_lt = true;

@@ -185,6 +185,7 @@ struct SelectOut {
 void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt,
                   const double* prob, bool transposed);
 void graph_set_lt(DevGraph& G, const float* w);
+void graph_set_lt_random(DevGraph& G, uint64_t seed);
 // device_gen.cu
 void graph_generate_rmat(DevGraph& G, Device& d, uint32_t scale, uint32_t ef, double a, double b, double c,
                          uint64_t seed, int weight_model, double p);

@@ -23,13 +23,17 @@ if cfg.get("device_gen"):
                                       p=cfg["weights"][1], device=dev)
 else:
     dg = im.DeviceGraph(bench.make_graph(im, cfg), transposed=False, device=dev)
+model = 0
+if "lt_seed" in cfg:
+    dg.set_lt_random(cfg["lt_seed"])
+    model = 1
 dev.synchronize()
 print(f"graph n={dg.n} m={dg.m} built in {time.perf_counter() - t:.2f}s", flush=True)
 dev.profile(True)
 for r in range(a.reps):
     dev.reset_stats()
     t = time.perf_counter()
-    out = im.run_device(dg, cfg["k"], epsilon=cfg["eps"], blocks=cfg["blocks"], mode=cfg["mode"], seed=42)
+    out = im.run_device(dg, cfg["k"], epsilon=cfg["eps"], blocks=cfg["blocks"], mode=cfg["mode"], seed=42, model=model)
     wall = time.perf_counter() - t
     st = dev.kernel_stats("sample")
     print(f"rep {r}: wall {wall:.2f}s theta {out['theta']} exit {out['exit_iteration']} est {out['estimation_samples']} "
