@@ -729,6 +729,7 @@ def run_device(dg: DeviceGraph, k: int, *, epsilon=0.5, blocks=8, mode="auto", s
             "compression_ratio": float(d[3]), "uncoded_vertex_fraction": float(d[4]),
             "phase_seconds": {"estimate": float(d[5]), "sample_encode": float(d[6]), "select": float(d[7]),
                               "total": float(d[8])},
+            "host_seconds": {"codebook": float(d[9]), "decode_table": float(d[10])},
             "characterized_mode": _MODE_NAME[int(i[0])], "mode": _MODE_NAME[int(i[1])],
             "mode_override": bool(i[2]),
             "block_sets": bs.tolist(), "block_raw": br.tolist(), "block_enc": be.tolist(),

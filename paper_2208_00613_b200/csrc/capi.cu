@@ -873,6 +873,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
             pool.count = pool.members = pool.edges = pool.arena_used = 0;
         }
         int mode = IMMX_MODE_RAW, char_mode = IMMX_MODE_RAW;
+        double t_codebook = 0.0, t_lut = 0.0;  // host: Huffman tree, decode table
         double skew = 0.0, dens = 0.0;
         HostCodebook cb;
         immx_store* store = nullptr;  // the device's run store (borrowed by the result)
@@ -905,14 +906,16 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     h1.exact(n);
                     CK(cudaMemsetAsync(h1.p, 0, n * 4, st));
                     pool_hist_dev(pool, lo, hi, h1.p);
-                    std::vector<unsigned int> f32(n);
-                    CK(cudaMemcpyAsync(f32.data(), h1.p, n * 4, cudaMemcpyDeviceToHost, st));
-                    CK(cudaStreamSynchronize(st));
-                    std::vector<uint64_t> f(f32.begin(), f32.end());
-                    cb = build_codebook_host(f.data(), n);
+                    const auto tc = Clock::now();
+                    std::vector<unsigned long long> leaves;
+                    codebook_leaves_dev(d, h1.p, n, leaves);
+                    cb = build_codebook_sorted(leaves.data(), leaves.size(), n);
+                    t_codebook = secs(tc);
+                    const auto tl = Clock::now();
                     std::vector<unsigned long long> lut;
                     uint32_t rb = 1;
                     build_decode_lut(cb, lut, rb);
+                    t_lut = secs(tl);
                     if (!d.run_store) d.run_store = new immx_store;
                     store = d.run_store;
                     store->s.count = store->s.total_words = store->s.total_copied = store->s.payload_bytes = 0;
@@ -1024,6 +1027,8 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         R->dd[6] = t_samp;
         R->dd[7] = t_sel;
         R->dd[8] = t_total;
+        R->dd[9] = t_codebook;
+        R->dd[10] = t_lut;
         R->ii[0] = char_mode;
         R->ii[1] = mode;
         R->ii[2] = cfg->mode >= 0 && cfg->mode != char_mode;

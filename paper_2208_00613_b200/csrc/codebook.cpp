@@ -7,114 +7,140 @@
 // the host (it is ~2% of the reference's time, and strictly sequential); the
 // device receives the per-vertex codes and a multi-level lookup table.
 #include <algorithm>
-#include <queue>
-#include <tuple>
 
 #include "internal.hpp"
 
 namespace immx_dev {
 
-HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n) {
+namespace {
+
+// The heap of huffman.cpp pops in ascending (frequency, min id) order; (freq, min id) is
+// unique per subtree, so that order is total.  With positive frequencies the popped
+// frequencies never decrease and every merged node outweighs both parts, so (i) merged
+// nodes are created in non-decreasing frequency and (ii) all merged nodes of frequency F
+// exist before the first pop of frequency F.  The same pop sequence therefore comes from
+// two queues -- the leaves sorted by (freq, id) and the merged nodes in creation order --
+// once each equal-frequency run of merged nodes is ordered by min id at its first use.
+// Linear after the leaf sort, which the device does (codebook_leaves_dev).
+template <class F, class I>
+HostCodebook merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id) {
     HostCodebook cb;
     cb.bits.assign(n, 0);
     cb.len.assign(n, 0);
-    using Entry = std::tuple<uint64_t, uint32_t, int32_t>;  // (freq, min id, node)
-    std::vector<Entry> heap_store;
-    std::priority_queue<Entry, std::vector<Entry>, std::greater<>> heap;
-    for (uint64_t v = 0; v < n; ++v) {
-        if (!freq[v]) continue;
-        HostCodebook::Node leaf;
-        leaf.symbol = (uint32_t)v;
-        cb.nodes.push_back(leaf);
-        heap.emplace(freq[v], (uint32_t)v, (int32_t)cb.nodes.size() - 1);
-        cb.coded++;
+    cb.children_first = true;
+    if (!L) fail(IMMX_ERUNTIME, "cannot build a codebook from an empty block");
+    if (L >= (1ULL << 31)) fail(IMMX_EINVAL, "too many coded symbols");
+    cb.coded = L;
+    cb.nodes.resize(L == 1 ? 2 : 2 * L - 1);
+    for (uint64_t i = 0; i < L; ++i) cb.nodes[i].symbol = leaf_id(i);
+    if (L == 1) {
+        cb.nodes[1].child[0] = 0;
+        cb.root = 1;
+        cb.bits[leaf_id(0)] = 0;  // a single symbol gets the 1-bit code "0"
+        cb.len[leaf_id(0)] = 1;
+        return cb;
     }
-    if (heap.empty()) fail(IMMX_ERUNTIME, "cannot build a codebook from an empty block");
-    if (heap.size() == 1) {
-        const int32_t leaf = std::get<2>(heap.top());
-        HostCodebook::Node root;
-        root.child[0] = leaf;
-        cb.nodes.push_back(root);
-        std::swap(cb.nodes.front(), cb.nodes.back());
-        cb.nodes.front().child[0] = (int32_t)cb.nodes.size() - 1;
-    } else {
-        while (heap.size() > 1) {
-            const Entry a = heap.top();
-            heap.pop();
-            const Entry b = heap.top();
-            heap.pop();
-            HostCodebook::Node inner;
-            inner.child[0] = std::get<2>(a);
-            inner.child[1] = std::get<2>(b);
-            cb.nodes.push_back(inner);
-            heap.emplace(std::get<0>(a) + std::get<0>(b), std::min(std::get<1>(a), std::get<1>(b)),
-                         (int32_t)cb.nodes.size() - 1);
-        }
-        const int32_t root = std::get<2>(heap.top());
-        if (root != 0) {
-            std::swap(cb.nodes[0], cb.nodes[root]);
-            for (auto& nd : cb.nodes)
-                for (int c = 0; c < 2; ++c) {
-                    if (nd.child[c] == 0) nd.child[c] = root;
-                    else if (nd.child[c] == root) nd.child[c] = 0;
-                }
-        }
-    }
-    // DFS code assignment (iterative; huffman.cpp:12-22)
-    struct Fr {
+    struct Q {
+        uint64_t f;
+        uint32_t minid;
         int32_t node;
-        uint64_t prefix;
-        uint32_t depth;
     };
-    std::vector<Fr> st{{0, 0, 0}};
-    while (!st.empty()) {
-        const Fr f = st.back();
-        st.pop_back();
-        const auto& nd = cb.nodes[f.node];
-        if (nd.child[0] < 0 && nd.child[1] < 0) {
-            cb.bits[nd.symbol] = f.prefix;
-            cb.len[nd.symbol] = (uint8_t)f.depth;
-            continue;
+    std::vector<Q> q;
+    q.reserve(L - 1);
+    uint64_t li = 0, qh = 0, ordered = 0;
+    auto pop = [&](uint64_t& f, uint32_t& minid) -> int32_t {
+        const bool have_leaf = li < L;
+        bool take_q = false;
+        if (qh < q.size() && (!have_leaf || leaf_freq(li) >= q[qh].f)) {
+            if (qh >= ordered) {  // first use of this equal-frequency run: order it by min id
+                uint64_t e = qh;
+                while (e < q.size() && q[e].f == q[qh].f) ++e;
+                auto lt = [](const Q& x, const Q& y) { return x.minid < y.minid; };
+                if (!std::is_sorted(q.begin() + qh, q.begin() + e, lt)) std::sort(q.begin() + qh, q.begin() + e, lt);
+                ordered = e;
+            }
+            take_q = !have_leaf || q[qh].f < leaf_freq(li) || q[qh].minid < leaf_id(li);
         }
-        if (f.depth >= 64) fail(IMMX_ERUNTIME, "huffman code longer than 64 bits");
-        if (nd.child[1] >= 0) st.push_back({nd.child[1], (f.prefix << 1) | 1u, f.depth + 1});
-        if (nd.child[0] >= 0) st.push_back({nd.child[0], f.prefix << 1, f.depth + 1});
+        if (take_q) {
+            f = q[qh].f;
+            minid = q[qh].minid;
+            return q[qh++].node;
+        }
+        f = leaf_freq(li);
+        minid = leaf_id(li);
+        return (int32_t)li++;
+    };
+    for (uint64_t k = 0; k + 1 < L; ++k) {
+        uint64_t fa, fb;
+        uint32_t ma, mb;
+        const int32_t a = pop(fa, ma);  // first popped: branch 0
+        const int32_t b = pop(fb, mb);
+        const int32_t u = (int32_t)(L + k);
+        cb.nodes[u].child[0] = a;
+        cb.nodes[u].child[1] = b;
+        q.push_back({fa + fb, std::min(ma, mb), u});
+    }
+    cb.root = (int32_t)(2 * L - 2);
+    // codes top-down: parents come after their children, so walk the merged nodes backwards
+    std::vector<uint64_t> pre(cb.nodes.size(), 0);
+    std::vector<uint8_t> dep(cb.nodes.size(), 0);
+    for (int64_t u = cb.root; u >= (int64_t)L; --u) {
+        if (dep[u] >= 64) fail(IMMX_ERUNTIME, "huffman code longer than 64 bits");
+        for (int c = 0; c < 2; ++c) {
+            const int32_t ch = cb.nodes[u].child[c];
+            pre[ch] = (pre[u] << 1) | (uint64_t)c;
+            dep[ch] = (uint8_t)(dep[u] + 1);
+        }
+    }
+    for (uint64_t i = 0; i < L; ++i) {
+        cb.bits[cb.nodes[i].symbol] = pre[i];
+        cb.len[cb.nodes[i].symbol] = dep[i];
     }
     return cb;
+}
+
+}  // namespace
+
+HostCodebook build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n) {
+    return merge_sorted(
+        count, n, [&](uint64_t i) { return (uint64_t)(leaves[i] >> 32); },
+        [&](uint64_t i) { return (uint32_t)(leaves[i] & 0xffffffffu); });
+}
+
+HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n) {
+    std::vector<uint32_t> ids;
+    for (uint64_t v = 0; v < n; ++v)
+        if (freq[v]) ids.push_back((uint32_t)v);
+    std::stable_sort(ids.begin(), ids.end(), [&](uint32_t a, uint32_t b) { return freq[a] < freq[b]; });
+    return merge_sorted(
+        ids.size(), n, [&](uint64_t i) { return freq[ids[i]]; }, [&](uint64_t i) { return ids[i]; });
 }
 
 // Multi-level decode table (entry layout: huffman.cu header).  Table widths: root
 // min(12, height), sub-tables min(8, height of the subtree below the boundary node).
 void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& lut, uint32_t& root_bits) {
     const size_t nn = cb.nodes.size();
-    // subtree heights (post-order, iterative)
+    // subtree heights: children before parents in one index sweep
     std::vector<uint32_t> height(nn, 0);
-    {
-        std::vector<std::pair<int32_t, bool>> st{{0, false}};
-        while (!st.empty()) {
-            auto [u, done] = st.back();
-            st.pop_back();
-            const auto& nd = cb.nodes[u];
-            if (done) {
-                uint32_t h = 0;
-                for (int c = 0; c < 2; ++c)
-                    if (nd.child[c] >= 0) h = std::max(h, height[nd.child[c]] + 1);
-                height[u] = h;
-                continue;
-            }
-            st.push_back({u, true});
-            for (int c = 0; c < 2; ++c)
-                if (nd.child[c] >= 0) st.push_back({nd.child[c], false});
-        }
-    }
+    auto upd = [&](size_t u) {
+        const auto& nd = cb.nodes[u];
+        uint32_t h = 0;
+        for (int c = 0; c < 2; ++c)
+            if (nd.child[c] >= 0) h = std::max(h, height[nd.child[c]] + 1);
+        height[u] = h;
+    };
+    if (cb.children_first)
+        for (size_t u = 0; u < nn; ++u) upd(u);
+    else
+        for (size_t u = nn; u-- > 0;) upd(u);
     lut.clear();
-    root_bits = std::max<uint32_t>(1, std::min<uint32_t>(12, height[0]));
+    root_bits = std::max<uint32_t>(1, std::min<uint32_t>(12, height[cb.root]));
     struct Job {
         int32_t node;
         uint32_t width;
         uint64_t offset;
     };
-    std::vector<Job> jobs{{0, root_bits, 0}};
+    std::vector<Job> jobs{{cb.root, root_bits, 0}};
     lut.assign((size_t)1 << root_bits, 0ULL);
     while (!jobs.empty()) {
         const Job jb = jobs.back();

@@ -280,10 +280,15 @@ struct HostCodebook {
     };
     std::vector<uint64_t> bits;
     std::vector<uint8_t> len;
-    std::vector<Node> nodes;  // nodes[0] = root
+    std::vector<Node> nodes;
+    int32_t root = 0;
+    bool children_first = false;  // true: every child index < its parent's (Huffman merge order)
     uint64_t coded = 0;
 };
 HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n);
+// leaves = the coded vertices as (freq << 32 | id), sorted ascending
+HostCodebook build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n);
+void codebook_leaves_dev(Device& d, const unsigned int* d_hist, uint64_t n, std::vector<unsigned long long>& leaves);
 void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& lut, uint32_t& root_bits);
 
 }  // namespace immx_dev

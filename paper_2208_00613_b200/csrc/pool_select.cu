@@ -38,6 +38,29 @@ __global__ void k_hist(const uint32_t* __restrict__ arena, const uint64_t* __res
     }
 }
 
+// Huffman leaves: every coded vertex as the key (freq << 32 | id), compacted in any order
+// (the sort that follows fixes it); the warp aggregates its slots with one atomic.
+__global__ void k_leaf_keys(const unsigned int* __restrict__ hist, uint64_t n, unsigned long long* __restrict__ keys,
+                            unsigned long long* __restrict__ count, unsigned int* __restrict__ maxf) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    unsigned int mf = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v - lane < n; v += stride) {
+        const unsigned int f = v < n ? hist[v] : 0u;
+        const uint32_t ball = __ballot_sync(FULL, f != 0);
+        if (!ball) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(ball));
+        base = __shfl_sync(FULL, base, 0);
+        if (f) {
+            keys[base + __popc(ball & ((1u << lane) - 1))] = ((unsigned long long)f << 32) | v;
+            mf = max(mf, f);
+        }
+    }
+    mf = __reduce_max_sync(FULL, mf);
+    if (lane == 0 && mf) atomicMax(maxf, mf);
+}
+
 __global__ void k_argmax(const unsigned int* __restrict__ hist, uint64_t n, unsigned long long* __restrict__ out) {
     unsigned long long best = 0;
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
@@ -163,6 +186,35 @@ void pool_hist_dev(const Pool& P, uint64_t lo, uint64_t hi, unsigned int* d_hist
     k_hist<<<grid_for((hi - lo) * 32, d), 256, 0, d.stream>>>(P.arena.p, P.off.p, P.len.p, lo, hi, d_hist);
     CK_LAUNCH("k_hist");
     d.kernel_launches++;
+}
+
+void codebook_leaves_dev(Device& d, const unsigned int* d_hist, uint64_t n, std::vector<unsigned long long>& leaves) {
+    const cudaStream_t s = d.stream;
+    DBuf<unsigned long long> k0, k1, cnt;
+    k0.exact(std::max<uint64_t>(n, 1));
+    k1.exact(std::max<uint64_t>(n, 1));
+    cnt.exact(2);
+    CK(cudaMemsetAsync(cnt.p, 0, 16, s));
+    k_leaf_keys<<<grid_for(n, d), 256, 0, s>>>(d_hist, n, k0.p, cnt.p, reinterpret_cast<unsigned int*>(cnt.p + 1));
+    CK_LAUNCH("k_leaf_keys");
+    d.kernel_launches++;
+    unsigned long long hc[2] = {0, 0};
+    CK(cudaMemcpyAsync(hc, cnt.p, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const uint64_t L = hc[0];
+    const uint32_t maxf = (uint32_t)hc[1];
+    leaves.resize(L);
+    if (!L) return;
+    int fbits = 1;
+    while (fbits < 32 && (maxf >> fbits)) ++fbits;
+    cub::DoubleBuffer<unsigned long long> db(k0.p, k1.p);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int64_t)L, 0, 32 + fbits, s);
+    d.tmp.reserve(tb, s, false);
+    CK(cub::DeviceRadixSort::SortKeys(d.tmp.p, tb, db, (int64_t)L, 0, 32 + fbits, s));
+    d.kernel_launches += 2 * ((32 + fbits + 7) / 8);
+    CK(cudaMemcpyAsync(leaves.data(), db.Current(), L * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
 }
 
 void argmax_dev(Device& d, const unsigned int* d_hist, uint64_t n, unsigned long long* d_key) {

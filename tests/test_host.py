@@ -86,9 +86,22 @@ def test_codebook_matches_oracle(im, orc):
         a, b = im.codebook_from_counts(f), orc.codebook(f)
         assert a.lens.tolist() == b.lens.tolist() and a.bits.tolist() == b.bits.tolist()
         assert a.coded_vertices == b.coded_vertices
+    # tie-heavy alphabets (the linear merge orders equal-frequency merged nodes by min id)
+    for trial in range(20):
+        f = rng.integers(0, 4, 3000 + 97 * trial)
+        f[rng.integers(0, f.size, 5)] = rng.integers(50, 5000, 5)
+        a, b = im.codebook_from_counts(f), orc.codebook(f)
+        assert a.lens.tolist() == b.lens.tolist() and a.bits.tolist() == b.bits.tolist()
     # a skewed alphabet with deep codes
     f = (2 ** np.arange(40)).astype(np.uint64)
     assert im.codebook_from_counts(f).lens.tolist() == orc.codebook(f).lens.tolist()
+    f = (2 ** np.arange(63)).astype(np.uint64)
+    assert im.codebook_from_counts(f).bits.tolist() == orc.codebook(f).bits.tolist()
+    fib = [1, 1]
+    while len(fib) < 70:
+        fib.append(fib[-1] + fib[-2])
+    with pytest.raises(RuntimeError):
+        im.codebook_from_counts(np.array(fib, dtype=np.uint64))
     with pytest.raises(RuntimeError):
         im.codebook_from_counts([0, 0, 0])
     assert im.codebook_from_counts([5, 2, 1]).dump() == "0 1 1\n1 2 01\n2 2 00\n"
