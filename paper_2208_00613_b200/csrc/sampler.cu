@@ -21,6 +21,10 @@
 
 #include <algorithm>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace immx_dev {
@@ -579,7 +583,7 @@ __device__ __forceinline__ void warp_prefix(const uint32_t* a, uint32_t w, uint3
 }
 
 template <int KIND, int PM, int NW, int U>
-__global__ void __launch_bounds__(NW * 32, 4) rrr_block_kernel(GView g, SampJob job, uint32_t vis_words) {
+__global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rrr_block_kernel(GView g, SampJob job, uint32_t vis_words) {
     extern __shared__ uint32_t dsm[];
     __shared__ BlkSmem<NW, U> sh;
     constexpr uint32_t NB = NW * 32;
@@ -954,17 +958,33 @@ struct Tier {
 constexpr int kBlkNW = 8;
 constexpr int kBlkU = IMMX_BLK_U;
 
+// CTA shape per tier: the small tiers run 4 CTAs of 8 warps per SM; the large-hash and
+// global-bitmap tiers hold the rare giant samples (one CTA per SM: 128 KB of hash), so they
+// take the whole SM's warps -- 32 warps, U = 2 (the static shared state must stay < 48 KB)
+#ifndef IMMX_BIG_NW
+#define IMMX_BIG_NW 32
+#endif
+#ifndef IMMX_BIG_U
+#define IMMX_BIG_U 2
+#endif
+template <int KIND>
+struct BlkShape {
+    static constexpr int NW = (KIND == kBHash15 || KIND == kBGlob) ? IMMX_BIG_NW : kBlkNW;
+    static constexpr int U = (KIND == kBHash15 || KIND == kBGlob) ? IMMX_BIG_U : kBlkU;
+};
+
 template <int KIND>
 uint32_t block_grid(Device& d, const Tier& tier, size_t smem) {
-    for (auto kern : {rrr_block_kernel<KIND, kProbGlobal, kBlkNW, kBlkU>, rrr_block_kernel<KIND, kProbRow, kBlkNW, kBlkU>,
-                      rrr_block_kernel<KIND, kProbEdge, kBlkNW, kBlkU>}) {
+    constexpr int NW = BlkShape<KIND>::NW, U = BlkShape<KIND>::U;
+    for (auto kern : {rrr_block_kernel<KIND, kProbGlobal, NW, U>, rrr_block_kernel<KIND, kProbRow, NW, U>,
+                      rrr_block_kernel<KIND, kProbEdge, NW, U>}) {
         if (smem > 48 * 1024)
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
-    auto kern = rrr_block_kernel<KIND, kProbEdge, kBlkNW, kBlkU>;
+    auto kern = rrr_block_kernel<KIND, kProbEdge, NW, U>;
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlkNW * 32, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem));
     if (per_sm < 1) fail(IMMX_ECUDA, "sampler tier does not fit on an SM");
     uint32_t blocks = (uint32_t)per_sm * (uint32_t)d.num_sms;
     if (tier.max_blocks) blocks = std::min(blocks, tier.max_blocks);
@@ -973,18 +993,18 @@ uint32_t block_grid(Device& d, const Tier& tier, size_t smem) {
 
 template <int KIND>
 void launch_block_tier(Device& d, const GView& gv, SampJob job, const Tier& tier, uint32_t nitems, uint32_t blocks) {
+    constexpr int NW = BlkShape<KIND>::NW, U = BlkShape<KIND>::U;
     const size_t smem = (size_t)tier.smem_words_per_warp * 4;
+    // bitmap words per CTA: the smem bitmap's size, or the per-CTA slice of the global one
+    const uint32_t words = KIND == kBGlob ? (uint32_t)((gv.n + 31) / 32) : tier.smem_words_per_warp;
     blocks = std::min<uint32_t>(blocks, std::max<uint32_t>(1, nitems));
     job.qcap = tier.qcap;
     if (gv.pmode == kProbGlobal)
-        rrr_block_kernel<KIND, kProbGlobal, kBlkNW, kBlkU><<<blocks, kBlkNW * 32, smem, d.stream>>>(
-            gv, job, tier.smem_words_per_warp);
+        rrr_block_kernel<KIND, kProbGlobal, NW, U><<<blocks, NW * 32, smem, d.stream>>>(gv, job, words);
     else if (gv.pmode == kProbRow)
-        rrr_block_kernel<KIND, kProbRow, kBlkNW, kBlkU><<<blocks, kBlkNW * 32, smem, d.stream>>>(
-            gv, job, tier.smem_words_per_warp);
+        rrr_block_kernel<KIND, kProbRow, NW, U><<<blocks, NW * 32, smem, d.stream>>>(gv, job, words);
     else
-        rrr_block_kernel<KIND, kProbEdge, kBlkNW, kBlkU><<<blocks, kBlkNW * 32, smem, d.stream>>>(
-            gv, job, tier.smem_words_per_warp);
+        rrr_block_kernel<KIND, kProbEdge, NW, U><<<blocks, NW * 32, smem, d.stream>>>(gv, job, words);
     CK_LAUNCH("rrr_block_kernel");
     d.kernel_launches++;
 }
@@ -1005,6 +1025,14 @@ void launch_tier(Device& d, const GView& gv, SampJob job, const Tier& tier, uint
     kern<<<blocks, wpb * 32, smem, d.stream>>>(gv, job, tier.smem_words_per_warp);
     CK_LAUNCH("rrr_kernel");
     d.kernel_launches++;
+}
+
+bool debug_tiers() {
+    static const bool on = [] {
+        const char* e = std::getenv("IMMX_DEBUG_TIERS");
+        return e && *e && *e != '0';
+    }();
+    return on;
 }
 
 uint32_t grid_warps(Device& d, const Tier& t) {
@@ -1143,6 +1171,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         job.gbits = gbits.p;
         KTimer kt;
         kt.start(&d, IMMX_KSTAT_SAMPLE);
+        const auto t_launch = std::chrono::steady_clock::now();
         if (tier.block) {
             switch (tier.kind) {
                 case kBBits: launch_block_tier<kBBits>(d, gv, job, tier, nitems, warps); break;
@@ -1167,6 +1196,11 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         edges += hctl->edges;
         members += hctl->members;
         const uint32_t n_ovf = hctl->n_ovf, n_nospace = hctl->n_nospace;
+        if (debug_tiers())
+            std::fprintf(stderr, "[immx sampler] tier %d%s items %u ovf %u nospace %u members %llu edges %llu %.3f ms\n",
+                         tier.kind, tier.block ? "b" : "w", nitems, n_ovf, n_nospace,
+                         (unsigned long long)hctl->members, (unsigned long long)hctl->edges,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_launch).count());
         {
             // algorithmic bytes of the samples this launch committed
             const uint64_t committed = nitems - n_ovf - n_nospace;

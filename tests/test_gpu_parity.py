@@ -84,17 +84,19 @@ def test_sample_duplicate_edges(im, orc):
     assert_same_sets(a[0], a[1], b[0], b[1])
 
 
-def test_sample_hash_tiers(im, orc):
-    # n large enough that the visited set is a shared-memory hash; high p forces big sets,
-    # which overflow tier 1 and are restarted on the bigger tiers
-    g = im.generate_rmat(19, 16, 0.57, 0.19, 0.19, 11)
-    im.assign_weights_f32(g, "uniform", 0.01)
+@pytest.mark.parametrize("p,lo,hi", [(0.006, 4096, 16384), (0.01, 16384, 1 << 30)])
+def test_sample_hash_tiers(im, orc, p, lo, hi):
+    # n = 2^20 > 2^19: the visited set is a shared-memory hash (tier 1: 4,096 members);
+    # p near the giant-component threshold makes some sets restart on the 32-warp large-hash
+    # tier (<= 16,384 members, p = .006) or on the per-CTA global bitmap (p = .01)
+    g = im.generate_rmat(20, 8, 0.57, 0.19, 0.19, 11)
+    im.assign_weights_f32(g, "uniform", p)
     gt = orc.transpose(csr_of(g))
-    a = orc.sample_block(gt, 300, 0, 5)
-    b = sample_dev(im, gt, 300, 0, 5)
+    a = orc.sample_block(gt, 600, 0, 5)
+    b = sample_dev(im, gt, 600, 0, 5)
     assert_same_sets(a[0], a[1], b[0], b[1])
     sizes = np.diff(a[0].astype(np.int64))
-    assert sizes.max() > 1024  # some samples escalated past tier 1
+    assert ((sizes > lo) & (sizes <= hi)).sum() >= 3
 
 
 def test_sample_rooted(im, orc):

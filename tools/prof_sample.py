@@ -25,10 +25,17 @@ def main():
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     t = time.time()
-    g = bench.make_graph(im, cfg)
-    print(f"graph {g} in {time.time() - t:.1f}s", flush=True)
     dev = im.default_device()
-    dg = im.DeviceGraph(g, transposed=False, device=dev)
+    if cfg.get("device_gen"):
+        gen = cfg["gen"]
+        dg = im.DeviceGraph.generate_rmat(gen[1], gen[2], 0.57, 0.19, 0.19, gen[3], weights=cfg["weights"][0],
+                                          p=cfg["weights"][1], device=dev)
+        dev.synchronize()
+        print(f"device graph n={dg.n} m={dg.m} in {time.time() - t:.1f}s", flush=True)
+    else:
+        g = bench.make_graph(im, cfg)
+        print(f"graph {g} in {time.time() - t:.1f}s", flush=True)
+        dg = im.DeviceGraph(g, transposed=False, device=dev)
     print("prob mode", dg.prob_mode, flush=True)
     for rep in range(a.reps):
         pool = im.Pool(dev)
