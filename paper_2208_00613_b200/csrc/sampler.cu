@@ -320,6 +320,7 @@ struct SampCtl {
     unsigned int pad;
     unsigned long long edges;
     unsigned long long members;
+    unsigned long long edges_abandoned;  // scanned by samples that moved to the next tier
 };
 
 struct SampJob {
@@ -936,6 +937,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
             }
         } else if (tid == 0) {
             job.ovf_list[atomicAdd(&job.ctl->n_ovf, 1u)] = j;
+            atomicAdd(&job.ctl->edges_abandoned, (unsigned long long)edges);
         }
         __syncthreads();
         vis.clear_members(q, qlen);
@@ -1197,9 +1199,10 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         members += hctl->members;
         const uint32_t n_ovf = hctl->n_ovf, n_nospace = hctl->n_nospace;
         if (debug_tiers())
-            std::fprintf(stderr, "[immx sampler] tier %d%s items %u ovf %u nospace %u members %llu edges %llu %.3f ms\n",
+            std::fprintf(stderr, "[immx sampler] tier %d%s items %u ovf %u nospace %u members %llu edges %llu abandoned %llu %.3f ms\n",
                          tier.kind, tier.block ? "b" : "w", nitems, n_ovf, n_nospace,
                          (unsigned long long)hctl->members, (unsigned long long)hctl->edges,
+                         (unsigned long long)hctl->edges_abandoned,
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_launch).count());
         {
             // algorithmic bytes of the samples this launch committed
