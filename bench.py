@@ -36,14 +36,14 @@ CONFIGS = {
                desc="ER n=10k m=100k seed 0, WC fl32, k=10 eps=0.5 b=10 huffman"),
     "c2": dict(gen=("rmat", 18, 16, 1), weights=("uniform", 0.01), k=50, eps=0.5, blocks=8, mode="huffman",
                desc="R-MAT scale 18 EF16 (.57,.19,.19) seed 1, IC p=fl32(0.01), k=50 eps=0.5 b=8 huffman"),
-    "c3": dict(gen=("rmat", 20, 16, 2), weights=("wc", 0.0), k=100, eps=0.5, blocks=8, mode="huffman",
+    "c3": dict(gen=("rmat", 20, 16, 2), weights=("wc", 0.0), k=100, eps=0.5, blocks=8, mode="hybrid",
                desc="R-MAT scale 20 EF16 seed 2, LT (in-weights U(0,1) normalised, f32, seed 3), k=100 eps=0.5 b=8 "
-                    "(hybrid degenerates to huffman: no set > n/32)", device_gen=True, lt_seed=3),
+                    "per-set hybrid (bitmap above n/32, Huffman otherwise)", device_gen=True, lt_seed=3),
     "c4": dict(gen=("rmat", 22, 24, 3), weights=("wc", 0.0), k=100, eps=0.13, blocks=8, mode="huffman",
                desc="R-MAT scale 22 EF24 seed 3, WC fl32, k=100 eps=0.13 b=8 huffman", device_gen=True),
-    "c5": dict(gen=("rmat", 25, 42, 4), weights=("wc", 0.0), k=50, eps=0.5, blocks=8, mode="huffman",
-               desc="R-MAT scale 25 EF42 seed 4, WC fl32, k=50 eps=0.5 b=8 huffman (hybrid degenerates: no set > n/32)",
-               device_gen=True),
+    "c5": dict(gen=("rmat", 25, 42, 4), weights=("wc", 0.0), k=50, eps=0.5, blocks=8, mode="hybrid",
+               desc="R-MAT scale 25 EF42 seed 4, WC fl32, k=50 eps=0.5 b=8 per-set hybrid (bitmap above n/32, "
+                    "Huffman otherwise)", device_gen=True),
 }
 METRIC = "RRR samples/s & achieved HBM GB/s at 1 B200; IMM end-to-end s; compress ratio"
 SEED = 42
@@ -341,6 +341,7 @@ def run_ours(args, cfg, rank, world, local):
                    "parallelism": f"replicas x{world}", "theta": r0["theta"], "reuse_pool": True},
         "imm_end_to_end_s": ms / args.steps / 1000.0,
         "compression_ratio": r0["compression_ratio"],
+        "dense_sets": r0.get("dense_sets", 0),
         "compression_ratio_device": r0["raw_bytes"] / r0["device_store_bytes"] if r0["device_store_bytes"] else None,
         "edges_examined_per_s": sum(x["edges_scanned"] for x in results) / (ms_local / 1000.0),
         "phase_seconds": r0["phase_seconds"],

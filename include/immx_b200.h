@@ -46,6 +46,8 @@ extern "C" {
 #define IMMX_MODE_HUFFMAN 0
 #define IMMX_MODE_BITMAP 1
 #define IMMX_MODE_RAW 2
+#define IMMX_MODE_HYBRID 3 /* per-set hybrid: Huffman store, n-bit bitmaps for sets above n/32
+                              (builder extension, never chosen by AUTO) */
 #define IMMX_MODE_AUTO (-1)
 
 #define IMMX_MODEL_IC 0 /* independent cascade: reverse BFS with per-edge coins */
@@ -201,6 +203,9 @@ IMMX_API int immx_store_encode(immx_store* s, const immx_pool* p, uint64_t lo, u
  * set-level decode_find API, including payloads a caller corrupted on purpose */
 IMMX_API int immx_store_append(immx_store* s, const uint8_t* bytes, uint64_t n_bytes, uint64_t bit_length,
                       const uint32_t* copied, uint64_t n_copied);
+/* per-set hybrid (IMMX_MODE_HYBRID): sets encoded after this call with 32*|R| > n become
+ * n-bit bitmaps (bit_length reads back as UINT64_MAX, 4*ceil(n/32) bytes, no copied) */
+IMMX_API int immx_store_set_hybrid(immx_store* s, int enable);
 /* *count sets, *payload = sum(ceil(bits/8) + 4*copied) (huffman.hpp:44), *device = bytes held */
 IMMX_API int immx_store_info(const immx_store* s, uint64_t* count, uint64_t* payload_bytes, uint64_t* device_bytes);
 /* D2H of sets [lo,hi): byte_off[hi-lo+1] (exclusive scan of ceil(bits/8)), bytes, bit_length,
@@ -249,9 +254,10 @@ IMMX_API int immx_run(const immx_graph* g, const immx_run_config* cfg, immx_resu
 /* scalars: u[0]=theta u[1]=estimation_samples u[2]=exit_iteration u[3]=blocks u[4]=raw_bytes
  *          u[5]=encoded_bytes u[6]=peak_bytes u[7]=padded u[8]=k u[9]=coded_vertices
  *          u[10]=device_store_bytes u[11]=samples_drawn u[12]=edges_scanned u[13]=members
+ *          u[14]=dense (bitmap) sets of a HYBRID store
  *          d[0]=covered_fraction d[1]=skewness d[2]=density d[3]=compression_ratio
  *          d[4]=uncoded_vertex_fraction d[5..8]=phase seconds (estimate, sample_encode,
- *          select, total; device-event timed)
+ *          select, total; device-event timed) d[9]=host codebook s d[10]=host decode-table s
  *          i[0]=characterized mode i[1]=mode i[2]=mode_overridden */
 IMMX_API int immx_result_scalars(const immx_result* r, uint64_t* u /*16*/, double* d /*12*/, int* i /*4*/);
 IMMX_API int immx_result_seeds(const immx_result* r, uint32_t* seeds, uint64_t* marginal, double* coverage);

@@ -622,7 +622,13 @@ OC_API int oc_decode_find(const oc_codebook* cb, const uint8_t* bytes, uint64_t 
     return 0;
 }
 
-/* An encoded store: per set, byte stream (enc_off into bytes), bit length, copied. */
+/* An encoded store: per set, byte stream (enc_off into bytes), bit length, copied.
+ * Per-set hybrid (builder extension, no reference counterpart -- SURVEY.md 8(f)3): with
+ * `hybrid` set, a set with more than n/32 members (32*|R| > n) is stored as an n-bit
+ * bitmap instead -- bit v = bit (v % 32) of little-endian u32 word v / 32, 4*ceil(n/32)
+ * bytes, bit length OC_DENSE, no copied members.  Such a set costs at most its raw bytes.
+ * Without dense sets the store is byte-identical to the Huffman one. */
+#define OC_DENSE UINT64_MAX
 typedef struct {
     uint64_t theta;
     uint64_t* enc_off; /* theta+1, byte offsets */
@@ -630,7 +636,12 @@ typedef struct {
     uint8_t* bytes;
     uint64_t* cp_off; /* theta+1 */
     uint32_t* copied;
+    int hybrid;
+    uint64_t n;
+    uint64_t dense_sets;
 } oc_store;
+
+static int oc_is_dense(const oc_store* s, uint64_t size) { return s->hybrid && 32 * size > s->n; }
 
 /* Encode sets [lo,hi) of a CSR with a single top into a store (appending). */
 static void oc_store_encode(oc_store* s, const oc_codebook* cb, const uint64_t* set_off,
@@ -638,6 +649,25 @@ static void oc_store_encode(oc_store* s, const oc_codebook* cb, const uint64_t* 
                             int64_t top, uint64_t* bytes_cap, uint64_t* cp_cap) {
     for (uint64_t j = lo; j < hi; ++j) {
         const uint64_t size = set_off[j + 1] - set_off[j];
+        if (oc_is_dense(s, size)) {
+            const uint64_t nb = 4 * ((s->n + 31) / 32);
+            const uint64_t need_b = s->enc_off[base + j - lo] + nb;
+            if (need_b > *bytes_cap) {
+                *bytes_cap = need_b * 2 + 64;
+                s->bytes = (uint8_t*)realloc(s->bytes, *bytes_cap);
+            }
+            uint8_t* out = s->bytes + s->enc_off[base + j - lo];
+            memset(out, 0, nb);
+            for (uint64_t p = set_off[j]; p < set_off[j + 1]; ++p) {
+                const uint32_t v = members[p];
+                out[4 * (v / 32) + (v % 32) / 8] |= (uint8_t)(1u << (v % 8));
+            }
+            s->bitlen[base + j - lo] = OC_DENSE;
+            s->enc_off[base + j - lo + 1] = need_b;
+            s->cp_off[base + j - lo + 1] = s->cp_off[base + j - lo];
+            s->dense_sets++;
+            continue;
+        }
         uint64_t bits_max = 0;
         for (uint64_t p = set_off[j]; p < set_off[j + 1]; ++p) bits_max += cb->code_len[members[p]];
         const uint64_t need_b = s->enc_off[base + j - lo] + (bits_max + 7) / 8;
@@ -692,6 +722,17 @@ OC_API uint32_t oc_select_huffman(const oc_codebook* cb, const oc_store* s, cons
         uint64_t newly = 0, maxd = 0;
         for (uint64_t j = 0; j < theta; ++j) {
             if (deleted[j]) continue;
+            if (s->bitlen[j] == OC_DENSE) { /* hybrid: test bit(pick); a miss recounts the bits */
+                const uint8_t* bm = s->bytes + s->enc_off[j];
+                if ((bm[4 * (pick / 32) + (pick % 32) / 8] >> (pick % 8)) & 1u) {
+                    deleted[j] = 1;
+                    newly++;
+                } else {
+                    for (uint64_t v = 0; v < n; ++v)
+                        if ((bm[4 * (v / 32) + (v % 32) / 8] >> (v % 8)) & 1u) hist[v]++;
+                }
+                continue;
+            }
             uint64_t nd = 0;
             const int f = oc_decode_find(cb, s->bytes + s->enc_off[j], s->enc_off[j + 1] - s->enc_off[j],
                                          s->bitlen[j], s->copied + s->cp_off[j],
@@ -791,7 +832,8 @@ OC_API uint32_t oc_select_bitmap(uint32_t* words, const uint64_t* word_base, con
 
 /* ------------------------------------------------------------- pipeline --- */
 /* proj/src/pipeline.cpp:47-178 run().  The graph passed is the FORWARD graph; the
- * pipeline transposes it.  mode: -1 auto, 0 huffman, 1 bitmap, 2 raw. */
+ * pipeline transposes it.  mode: -1 auto, 0 huffman, 1 bitmap, 2 raw, 3 per-set hybrid
+ * (Huffman store with n-bit bitmaps for sets above n/32 -- builder extension). */
 typedef struct {
     /* plan */
     uint64_t theta, estimation_samples;
@@ -888,7 +930,7 @@ OC_API oc_run_result* oc_run(uint64_t n, uint64_t m, const uint64_t* off, const 
             mode = mode_override >= 0 ? mode_override : R->char_mode;
             R->mode_overridden = mode_override >= 0 && mode_override != R->char_mode;
             R->mode = mode;
-            if (mode == 0) {
+            if (mode == 0 || mode == 3) {
                 uint64_t* f = (uint64_t*)calloc(n, sizeof(uint64_t));
                 for (uint64_t p = 0; p < blk->total; ++p) f[blk->members[p]]++;
                 R->cb = oc_build_codebook(f, n);
@@ -897,10 +939,12 @@ OC_API oc_run_result* oc_run(uint64_t n, uint64_t m, const uint64_t* off, const 
                 R->store.enc_off = (uint64_t*)calloc(theta + 1, sizeof(uint64_t));
                 R->store.bitlen = (uint64_t*)calloc(theta ? theta : 1, sizeof(uint64_t));
                 R->store.cp_off = (uint64_t*)calloc(theta + 1, sizeof(uint64_t));
+                R->store.hybrid = mode == 3;
+                R->store.n = n;
             }
         }
         uint64_t enc = 0;
-        if (mode == 0) { /* pipeline.cpp:106-118 */
+        if (mode == 0 || mode == 3) { /* pipeline.cpp:106-118 (3: per-set hybrid) */
             for (uint64_t p = 0; p < blk->total; ++p) hist[blk->members[p]]++;
             const uint32_t top = oc_table_argmax(hist, n);
             R->tops[i - 1] = top;
@@ -937,7 +981,7 @@ OC_API oc_run_result* oc_run(uint64_t n, uint64_t m, const uint64_t* off, const 
     }
     R->compression_ratio =
         R->encoded_bytes == 0 ? 1.0 : (double)R->raw_bytes / (double)R->encoded_bytes;
-    if (mode == 0) {
+    if (mode == 0 || mode == 3) {
         uint64_t unc = 0;
         for (uint64_t v = 0; v < n; ++v)
             if (hist[v] > 0 && R->cb->code_len[v] == 0) unc++;
@@ -951,7 +995,7 @@ OC_API oc_run_result* oc_run(uint64_t n, uint64_t m, const uint64_t* off, const 
     CKPT();
     if (mode == 2) {
         R->padded = oc_select_raw(R->set_off, R->members, theta, n, k, R->seeds, R->marginal, R->coverage);
-    } else if (mode == 0) {
+    } else if (mode == 0 || mode == 3) {
         uint64_t* maxd = (uint64_t*)calloc(k, sizeof(uint64_t));
         R->padded = oc_select_huffman(R->cb, &R->store, hist, n, k, R->seeds, R->marginal,
                                       R->coverage, maxd);
@@ -993,6 +1037,7 @@ OC_API void oc_run_scalars(const oc_run_result* R, uint64_t* u, double* d, int* 
     u[10] = R->store.theta ? R->store.enc_off[R->store.theta] : 0;
     u[11] = R->store.theta ? R->store.cp_off[R->store.theta] : 0;
     u[12] = R->set_off ? R->set_off[R->theta] : 0;
+    u[13] = R->store.dense_sets;
     d[0] = R->covered_fraction;
     d[1] = R->skewness;
     d[2] = R->density;

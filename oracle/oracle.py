@@ -26,7 +26,7 @@ f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 
-MODES = {"huffman": 0, "bitmap": 1, "raw": 2}
+MODES = {"huffman": 0, "bitmap": 1, "raw": 2, "hybrid": 3}  # 3: builder extension (per-set hybrid)
 MODE_NAMES = {v: k for k, v in MODES.items()}
 
 
@@ -259,7 +259,7 @@ class Oracle:
                                  k, epsilon, blocks, m, seed, workers)
         else:
             h = self.L.oc_run(g.n, g.m, g.off, _nz32(g.tgt), _nz64(g.prob), k, epsilon, blocks, m, seed, workers)
-        u = np.zeros(13, np.uint64)
+        u = np.zeros(14, np.uint64)
         d = np.zeros(5, np.float64)
         i = np.zeros(3, np.int32)
         self.L.oc_run_scalars(h, u, d, i)
@@ -275,7 +275,7 @@ class Oracle:
             "seeds": seeds.tolist(), "marginal": marg.tolist(), "coverage": cov.tolist(), "padded": int(u[7]),
             "theta": int(u[0]), "estimation_samples": int(u[1]), "exit_iteration": int(u[2]), "blocks": b,
             "raw_bytes": int(u[4]), "encoded_bytes": int(u[5]), "peak_bytes": int(u[6]),
-            "coded_vertices": int(u[9]),
+            "coded_vertices": int(u[9]), "dense_sets": int(u[13]),
             "covered_fraction": float(d[0]), "skewness": float(d[1]), "density": float(d[2]),
             "compression_ratio": float(d[3]), "uncoded_vertex_fraction": float(d[4]),
             "characterized_mode": MODE_NAMES[int(i[0])], "mode": MODE_NAMES[int(i[1])],
@@ -287,7 +287,7 @@ class Oracle:
             mem = np.zeros(max(int(u[12]), 1), np.uint32)
             self.L.oc_run_pool(h, so, mem)
             out["pool"] = (so, mem[: int(u[12])])
-        if want_store and out["mode"] == "huffman":
+        if want_store and out["mode"] in ("huffman", "hybrid"):
             t = out["theta"]
             eo, bl, cp = np.zeros(t + 1, np.uint64), np.zeros(t, np.uint64), np.zeros(t + 1, np.uint64)
             by = np.zeros(max(int(u[10]), 1), np.uint8)

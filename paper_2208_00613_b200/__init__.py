@@ -33,7 +33,9 @@ __all__ = [
     "Device", "default_device", "generate_rmat", "generate_er", "DeviceGraph", "Pool", "run_device",
 ]
 
-_MODE_ID = {"huffman": _capi.MODE_HUFFMAN, "bitmap": _capi.MODE_BITMAP, "raw": _capi.MODE_RAW}
+# "hybrid" (builder extension): the Huffman store with n-bit bitmaps for sets above n/32
+_MODE_ID = {"huffman": _capi.MODE_HUFFMAN, "bitmap": _capi.MODE_BITMAP, "raw": _capi.MODE_RAW,
+            "hybrid": _capi.MODE_HYBRID}
 _MODE_NAME = {v: k for k, v in _MODE_ID.items()}
 
 
@@ -483,6 +485,20 @@ class Store:
         except Exception:
             pass
 
+    def decode_find(self, j: int, top: int):
+        """huffman.cpp:129-158 on stored set j -> (found, decoded); a hybrid bitmap set is a
+        bit test and decodes nothing."""
+        found, nd = C.c_int(), C.c_uint64()
+        bo, _, bl, _, _ = self.read(j, j + 1)
+        cap = 1 if int(bl[0]) == 2 ** 64 - 1 else int(bl[0]) + 1
+        dec = np.zeros(cap, np.uint32)
+        check(lib.immx_store_decode_find(self.h, j, top, C.byref(found), ptr(dec, C.c_uint32), C.byref(nd)))
+        return bool(found.value), dec[: nd.value].tolist()
+
+    def set_hybrid(self, enable: bool = True):
+        """Per-set hybrid (extension): later-encoded sets above n/32 become n-bit bitmaps."""
+        check(lib.immx_store_set_hybrid(self.h, int(bool(enable))))
+
     def info(self):
         c, p, d = C.c_uint64(), C.c_uint64(), C.c_uint64()
         check(lib.immx_store_info(self.h, C.byref(c), C.byref(p), C.byref(d)))
@@ -724,7 +740,7 @@ def run_device(dg: DeviceGraph, k: int, *, epsilon=0.5, blocks=8, mode="auto", s
             "theta": int(u[0]), "estimation_samples": int(u[1]), "exit_iteration": int(u[2]), "blocks": b,
             "raw_bytes": int(u[4]), "encoded_bytes": int(u[5]), "peak_bytes": int(u[6]),
             "coded_vertices": int(u[9]), "device_store_bytes": int(u[10]), "samples_drawn": int(u[11]),
-            "edges_scanned": int(u[12]), "pool_members": int(u[13]),
+            "edges_scanned": int(u[12]), "pool_members": int(u[13]), "dense_sets": int(u[14]),
             "covered_fraction": float(d[0]), "skewness": float(d[1]), "density": float(d[2]),
             "compression_ratio": float(d[3]), "uncoded_vertex_fraction": float(d[4]),
             "phase_seconds": {"estimate": float(d[5]), "sample_encode": float(d[6]), "select": float(d[7]),
@@ -735,7 +751,8 @@ def run_device(dg: DeviceGraph, k: int, *, epsilon=0.5, blocks=8, mode="auto", s
             "block_sets": bs.tolist(), "block_raw": br.tolist(), "block_enc": be.tolist(),
         }
         if keep:
-            out["_store"] = Store(None, dg.device, handle=lib.immx_result_store(h)) if out["mode"] == "huffman" else None
+            out["_store"] = (Store(None, dg.device, handle=lib.immx_result_store(h))
+                             if out["mode"] in ("huffman", "hybrid") else None)
         return out
     finally:
         if not keep:
@@ -787,7 +804,8 @@ def run(graph: Graph, k: int, *, epsilon=0.5, blocks=8, mode="auto", seed=42, wo
         "original_ids": ids.tolist(),
         "rss_bytes": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss * 1024,
         "device": {"samples_drawn": r["samples_drawn"], "edges_scanned": r["edges_scanned"],
-                   "device_store_bytes": r["device_store_bytes"], "coded_vertices": r["coded_vertices"]},
+                   "device_store_bytes": r["device_store_bytes"], "coded_vertices": r["coded_vertices"],
+                   "dense_sets": r["dense_sets"]},
     }
     return {"seeds": r["seeds"], "marginal": r["marginal"], "coverage": r["coverage"], "padded": r["padded"],
             "seed_ids": [int(ids[s]) for s in r["seeds"]], "stats": stats}

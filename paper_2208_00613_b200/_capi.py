@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libimmx_b200.so")
 
 OK, EINVAL, ERUNTIME, ERANGE, ECUDA = 0, 1, 2, 3, 4
-MODE_HUFFMAN, MODE_BITMAP, MODE_RAW, MODE_AUTO = 0, 1, 2, -1
+MODE_HUFFMAN, MODE_BITMAP, MODE_RAW, MODE_HYBRID, MODE_AUTO = 0, 1, 2, 3, -1
 MODEL_IC, MODEL_LT = 0, 1
 KSTAT = {"sample": 0, "encode": 1, "hselect": 2, "rselect": 3, "argmax": 4}
 
@@ -107,6 +107,7 @@ SIGNATURES = {
     "immx_store_encode": (I, [P, P, u64, u64, i64]),
     "immx_store_append": (I, [P, pu8, u64, u64, pu32, u64]),
     "immx_store_info": (I, [P, pu64, pu64, pu64]),
+    "immx_store_set_hybrid": (I, [P, C.c_int]),
     "immx_store_read": (I, [P, u64, u64, pu64, pu8, pu64, pu64, pu32]),
     "immx_store_decode_find": (I, [P, u64, u32, pint, pu32, pu64]),
     "immx_select_huffman": (I, [P, pu64, u32, pu32, pu64, pdbl, pu32, pu64]),

@@ -691,6 +691,12 @@ int immx_store_append(immx_store* s, const uint8_t* bytes, uint64_t n_bytes, uin
         store_append_host(s->s, bytes, n_bytes, bit_length, copied, n_copied);
     });
 }
+int immx_store_set_hybrid(immx_store* s, int enable) {
+    return guard([&] {
+        need(s, "store");
+        s->s.hybrid = enable != 0;
+    });
+}
 int immx_store_info(const immx_store* s, uint64_t* count, uint64_t* payload, uint64_t* device_bytes) {
     return guard([&] {
         need(s, "store");
@@ -829,7 +835,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         if (k < 1 || k >= n) fail(IMMX_EINVAL, "k must satisfy 1 <= k < n");
         if (!(cfg->epsilon > 0.0)) fail(IMMX_EINVAL, "epsilon must be > 0");
         if (cfg->blocks < 2) fail(IMMX_EINVAL, "block count must be >= 2");
-        if (cfg->mode < -1 || cfg->mode > 2) fail(IMMX_EINVAL, "unknown mode");
+        if (cfg->mode < -1 || cfg->mode > IMMX_MODE_HYBRID) fail(IMMX_EINVAL, "unknown mode");
         const int workers = std::max(cfg->workers, 1);
         using Clock = std::chrono::steady_clock;
         auto secs = [](Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); };
@@ -901,7 +907,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                 dens = density_host(sizes.data(), count, n);
                 char_mode = choose_encoding_host(skew, dens);
                 mode = cfg->mode >= 0 ? cfg->mode : char_mode;
-                if (mode == IMMX_MODE_HUFFMAN) {
+                if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {
                     DBuf<unsigned int> h1;
                     h1.exact(n);
                     CK(cudaMemsetAsync(h1.p, 0, n * 4, st));
@@ -919,6 +925,8 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     if (!d.run_store) d.run_store = new immx_store;
                     store = d.run_store;
                     store->s.count = store->s.total_words = store->s.total_copied = store->s.payload_bytes = 0;
+                    store->s.dense_count = 0;
+                    store->s.hybrid = mode == IMMX_MODE_HYBRID;
                     store_set_codes(store->s, d, n, cb.bits.data(), cb.len.data(), lut, rb);
                 } else if (mode == IMMX_MODE_BITMAP) {
                     bm.reset(new immx_bitmap);
@@ -927,7 +935,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                 }
             }
             uint64_t enc = 0;
-            if (mode == IMMX_MODE_HUFFMAN) {  // pipeline.cpp:106-118
+            if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {  // pipeline.cpp:106-118
                 pool_hist_dev(pool, lo, hi, hist.p);
                 unsigned long long* key = d.scal.p + 60;
                 CK(cudaMemsetAsync(key, 0, 8, st));
@@ -960,7 +968,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         }
         const double ratio = enc_total == 0 ? 1.0 : (double)raw_total / (double)enc_total;
         double uncoded = 0.0;
-        if (mode == IMMX_MODE_HUFFMAN) {
+        if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {
             std::vector<unsigned int> hh(n);
             CK(cudaMemcpyAsync(hh.data(), hist.p, n * 4, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
@@ -977,7 +985,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         SelectOut sel;
         if (mode == IMMX_MODE_RAW) {
             select_raw_dev(pool, n, k, sel);
-        } else if (mode == IMMX_MODE_HUFFMAN) {
+        } else if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {
             std::vector<uint64_t> md;
             select_huffman_dev(store->s, hist.p, k, sel, &md);
             for (uint32_t r = 0; r < k; ++r) {
@@ -1018,6 +1026,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         R->u[11] = samples_drawn;
         R->u[12] = pool.edges;
         R->u[13] = pool.members;
+        R->u[14] = store ? store->s.dense_count : 0;
         R->dd[0] = plan.covered_fraction;
         R->dd[1] = skew;
         R->dd[2] = dens;

@@ -38,7 +38,8 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
                            const uint32_t* __restrict__ len, uint64_t lo, uint64_t hi,
                            const uint8_t* __restrict__ code_len, int64_t top, uint32_t* __restrict__ bits,
                            uint64_t* __restrict__ nwords, uint64_t* __restrict__ ncopied, uint8_t* __restrict__ swap,
-                           unsigned long long* __restrict__ payload) {
+                           unsigned long long* __restrict__ payload, uint64_t dense_n, uint64_t base,
+                           uint32_t* __restrict__ dense_ids, unsigned long long* __restrict__ dense_cnt) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -46,6 +47,19 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
     for (uint64_t j = lo + w; j < hi; j += nw) {
         const uint64_t b = off[j];
         const uint32_t l = len[j];
+        if (dense_n && 32ull * l > dense_n) {  // hybrid: an n-bit bitmap
+            if (lane == 0) {
+                const uint64_t k = j - lo;
+                const uint64_t nwd = (dense_n + 31) / 32;
+                bits[k] = kDenseBits;
+                nwords[k] = nwd;
+                ncopied[k] = 0;
+                swap[k] = 0;
+                atomicAdd(payload, (unsigned long long)(4 * nwd));
+                dense_ids[atomicAdd(dense_cnt, 1ull)] = (uint32_t)(base + k);
+            }
+            continue;
+        }
         uint32_t nb = 0, nc = 0;
         bool has_top = false;
         for (uint32_t i = lane; i < l; i += 32) {
@@ -89,7 +103,7 @@ __global__ void k_enc_pack(const uint32_t* __restrict__ arena, const uint64_t* _
                            const uint64_t* __restrict__ code_bits, const uint8_t* __restrict__ code_len, int64_t top,
                            const uint8_t* __restrict__ swap, const uint64_t* __restrict__ woff,
                            const uint64_t* __restrict__ coff, uint32_t* __restrict__ words,
-                           uint32_t* __restrict__ copied) {
+                           uint32_t* __restrict__ copied, const uint32_t* __restrict__ bits) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t lt = lanemask_lt();
     const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -99,6 +113,13 @@ __global__ void k_enc_pack(const uint32_t* __restrict__ arena, const uint64_t* _
         const uint64_t b = off[j];
         const uint32_t l = len[j];
         uint32_t* out = words + woff[k];
+        if (bits[k] == kDenseBits) {
+            for (uint32_t i = lane; i < l; i += 32) {
+                const uint32_t v = arena[b + i];
+                atomicOr(&out[v >> 5], 1u << (v & 31));
+            }
+            continue;
+        }
         uint32_t* cp = copied + coff[k];
         const bool sw = swap[k];
         uint64_t bitpos = 0;
@@ -197,6 +218,7 @@ __global__ void k_huff_round(const uint32_t* __restrict__ words, const uint64_t*
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += (uint64_t)gridDim.x * blockDim.x) {
         if (deleted[j]) continue;
         const uint32_t nbits = bits[j];
+        if (nbits == kDenseBits) continue;  // hybrid bitmap sets: k_dense_round
         BitReader br;
         br.init(words + woff[j]);
         uint32_t pos = 0, nd = 0;
@@ -237,6 +259,36 @@ __global__ void k_huff_round(const uint32_t* __restrict__ words, const uint64_t*
     }
     if (local_max) atomicMax(maxdec, (unsigned long long)local_max);
     if (local_bytes) atomicAdd(alg_bytes, (unsigned long long)local_bytes);
+}
+
+// select round over the hybrid store's bitmap sets: CTA per set, test bit(pick); a covered
+// set subtracts every set bit (the same table the reference's recount of the misses gives)
+__global__ void k_dense_round(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
+                              const uint32_t* __restrict__ ids, uint64_t nd, uint64_t nwd,
+                              const uint32_t* __restrict__ cover_pick, uint8_t* __restrict__ deleted,
+                              unsigned int* __restrict__ hist, unsigned long long* __restrict__ alg_bytes) {
+    const uint32_t pick = *cover_pick;
+    if (pick == 0xffffffffu) return;
+    uint64_t local_bytes = 0;
+    for (uint64_t x = blockIdx.x; x < nd; x += gridDim.x) {
+        const uint32_t j = ids[x];
+        if (deleted[j]) continue;  // uniform over the CTA
+        const uint32_t* bm = words + woff[j];
+        local_bytes += 4;
+        if (!((__ldg(bm + (pick >> 5)) >> (pick & 31)) & 1u)) continue;
+        local_bytes += 4 * nwd;
+        for (uint64_t i = threadIdx.x; i < nwd; i += blockDim.x) {
+            uint32_t m = __ldg(bm + i);
+            while (m) {
+                const uint32_t b = __ffs(m) - 1;
+                m &= m - 1;
+                atomicSub(&hist[(uint32_t)(i * 32 + b)], 1u);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) deleted[j] = 1;
+    }
+    if (threadIdx.x == 0 && local_bytes) atomicAdd(alg_bytes, (unsigned long long)local_bytes);
 }
 
 // decode_find on one set with every reference corruption check (huffman.cpp:129-158)
@@ -357,8 +409,14 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     CK(cudaMemsetAsync(d_payload, 0, 8, s));
     KTimer kt_size, kt_pack;
     kt_size.start(&d, IMMX_KSTAT_ENCODE);
+    unsigned long long* d_dense = d.scal.p + 17;
+    if (S.hybrid) {
+        S.dense_ids.reserve(S.dense_count + cnt, s);
+        CK(cudaMemcpyAsync(d_dense, &S.dense_count, 8, cudaMemcpyHostToDevice, s));
+    }
     k_enc_size<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_len.p, top,
-                                                   S.bits.p + base, nwords.p, ncp.p, swap.p, d_payload);
+                                                   S.bits.p + base, nwords.p, ncp.p, swap.p, d_payload,
+                                                   S.hybrid ? S.n : 0, base, S.dense_ids.p, d_dense);
     kt_size.stop();
     CK_LAUNCH("k_enc_size");
     d.kernel_launches++;
@@ -373,9 +431,19 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     uint64_t add[2];
     CK(cudaMemcpyAsync(&add[0], S.woff.p + base + cnt, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&add[1], S.coff.p + base + cnt, 8, cudaMemcpyDeviceToHost, s));
-    unsigned long long payload = 0;
+    unsigned long long payload = 0, dense_total = S.dense_count;
     CK(cudaMemcpyAsync(&payload, d_payload, 8, cudaMemcpyDeviceToHost, s));
+    if (S.hybrid) CK(cudaMemcpyAsync(&dense_total, d_dense, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (S.hybrid && dense_total > S.dense_count) {
+        // the kernel appended the block's dense ids in arbitrary order: sort them (cheap, rare)
+        std::vector<uint32_t> ids(dense_total - S.dense_count);
+        CK(cudaMemcpyAsync(ids.data(), S.dense_ids.p + S.dense_count, ids.size() * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::sort(ids.begin(), ids.end());
+        CK(cudaMemcpyAsync(S.dense_ids.p + S.dense_count, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, s));
+    }
+    S.dense_count = dense_total;
     // shift the block's offsets by the store totals (they were scanned from 0)
     const uint64_t w_total = S.total_words, c_total = S.total_copied;
     if (w_total || c_total) {
@@ -390,7 +458,7 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     kt_pack.start(&d, IMMX_KSTAT_ENCODE);
     k_enc_pack<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_bits.p, S.code_len.p,
                                                    top, swap.p, S.woff.p + base, S.coff.p + base, S.words.p,
-                                                   S.copied.p);
+                                                   S.copied.p, S.bits.p + base);
     kt_pack.stop();
     CK_LAUNCH("k_enc_pack");
     d.kernel_launches++;
@@ -450,6 +518,14 @@ int store_decode_find(const Store& S, uint64_t j, uint32_t top, std::vector<uint
     CK(cudaMemcpyAsync(co, S.coff.p + j, 16, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&nbits, S.bits.p + j, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (nbits == kDenseBits) {  // hybrid bitmap set: a bit test, nothing decoded
+        if (top >= S.n) return 0;
+        uint32_t word = 0;
+        CK(cudaMemcpyAsync(&word, S.words.p + wo[0] + top / 32, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        decoded.clear();
+        return (int)((word >> (top % 32)) & 1u);
+    }
     DBuf<uint32_t> dec;
     dec.exact((uint64_t)nbits + 1);
     long long* out = reinterpret_cast<long long*>(d.scal.p + 24);
@@ -501,6 +577,12 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
         kt[r].start(&d, IMMX_KSTAT_HSELECT);
         k_huff_round<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, theta, S.lut.p,
                                          S.lut_root_bits, ctl.p, deleted.p, d_hist, mdec.p + r, rbytes.p + r);
+        if (S.dense_count) {
+            k_dense_round<<<(unsigned)std::min<uint64_t>(S.dense_count, (uint64_t)d.num_sms * 8), 256, 0, s>>>(
+                S.words.p, S.woff.p, S.dense_ids.p, S.dense_count, (n + 31) / 32, ctl.p, deleted.p, d_hist,
+                rbytes.p + r);
+            d.kernel_launches++;
+        }
         kt[r].stop();
         CK_LAUNCH("select_huffman round");
         d.kernel_launches += 2;
@@ -532,11 +614,12 @@ void store_read_host(const Store& S, uint64_t lo, uint64_t hi, uint64_t* byte_of
     CK(cudaMemcpyAsync(co.data(), S.coff.p + lo, (cnt + 1) * 8, cudaMemcpyDeviceToHost, s));
     if (cnt) CK(cudaMemcpyAsync(nb.data(), S.bits.p + lo, cnt * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const uint64_t dense_bytes = 4 * ((S.n + 31) / 32);
     if (bit_length)
-        for (uint64_t j = 0; j < cnt; ++j) bit_length[j] = nb[j];
+        for (uint64_t j = 0; j < cnt; ++j) bit_length[j] = nb[j] == kDenseBits ? UINT64_MAX : nb[j];
     if (byte_off || bytes) {
         std::vector<uint64_t> bo(cnt + 1, 0);
-        for (uint64_t j = 0; j < cnt; ++j) bo[j + 1] = bo[j] + (nb[j] + 7) / 8;
+        for (uint64_t j = 0; j < cnt; ++j) bo[j + 1] = bo[j] + (nb[j] == kDenseBits ? dense_bytes : (nb[j] + 7) / 8);
         if (byte_off) std::memcpy(byte_off, bo.data(), (cnt + 1) * 8);
         if (bytes && cnt) {
             std::vector<uint32_t> w(wo[cnt] - wo[0]);

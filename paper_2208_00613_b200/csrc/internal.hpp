@@ -170,7 +170,13 @@ struct Store {
     DBuf<uint32_t> copied;
     uint64_t total_words = 0, total_copied = 0;
     uint64_t payload_bytes = 0;  // reference formula: sum ceil(bits/8) + 4*copied
+    // per-set hybrid (builder extension): sets with 32*|R| > n are n-bit bitmaps in `words`
+    // (bits[j] = kDenseBits, ceil(n/32) LSB-first words, no copied members)
+    bool hybrid = false;
+    uint64_t dense_count = 0;
+    DBuf<uint32_t> dense_ids;  // store indices of the dense sets
 };
+constexpr uint32_t kDenseBits = 0xffffffffu;
 
 
 // ---------------------------------------------------------------- device operations ----

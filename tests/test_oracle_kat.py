@@ -280,3 +280,60 @@ def test_pipeline_modes_agree(orc):
         g = orc.assign_weights(random_graph(rng, 40 + 20 * trial, 300 + 100 * trial), "wc")
         res = [orc.run(g, 5, 0.5, 4, m, 100 + trial)["seeds"] for m in ("raw", "huffman", "bitmap")]
         assert res[0] == res[1] == res[2]
+
+
+def _dense_graph(rng, n, m, p):
+    g = random_graph(rng, n, m)
+    return orc_assign_uniform(g, p)
+
+
+def orc_assign_uniform(g, p):
+    from oracle.oracle import CSR
+    return CSR(g.n, g.off, g.tgt, np.full(g.m, p, np.float64))
+
+
+def test_hybrid_store_oracle(orc):
+    # per-set hybrid (builder extension, self-pinned): sets above n/32 become n-bit bitmaps;
+    # the greedy is the same function of the sets, so seeds / marginals / coverage equal the
+    # raw and Huffman modes; Huffman-coded sets keep the Huffman mode's exact bytes
+    rng = np.random.default_rng(5)
+    for trial in range(3):
+        g = _dense_graph(rng, 300 + 50 * trial, 3000, 0.3)
+        runs = {m: orc.run(g, 6, 0.5, 4, m, 7 + trial, want_store=True, want_pool=True)
+                for m in ("raw", "huffman", "hybrid")}
+        hy, hu = runs["hybrid"], runs["huffman"]
+        assert hy["dense_sets"] > 0 and hu["dense_sets"] == 0
+        for key in ("seeds", "marginal", "coverage"):
+            assert hy[key] == hu[key] == runs["raw"][key], key
+        so, mem = hy["pool"]
+        n = g.n
+        nb = 4 * ((n + 31) // 32)
+        st, su = hy["store"], hu["store"]
+        dense = 0
+        enc = 0
+        for j in range(hy["theta"]):
+            members = mem[int(so[j]):int(so[j + 1])]
+            a0, a1 = int(st["enc_off"][j]), int(st["enc_off"][j + 1])
+            if 32 * members.size > n:
+                dense += 1
+                assert int(st["bit_length"][j]) == 2 ** 64 - 1 and a1 - a0 == nb
+                bm = np.frombuffer(st["bytes"][a0:a1].tobytes(), "<u4")
+                got = np.nonzero((bm[np.arange(n) // 32] >> (np.arange(n) % 32)) & 1)[0]
+                assert got.tolist() == sorted(members.tolist())
+                assert st["cp_off"][j + 1] == st["cp_off"][j]
+                enc += nb
+            else:
+                b0, b1 = int(su["enc_off"][j]), int(su["enc_off"][j + 1])
+                assert st["bytes"][a0:a1].tobytes() == su["bytes"][b0:b1].tobytes()
+                assert st["bit_length"][j] == su["bit_length"][j]
+                c = st["copied"][int(st["cp_off"][j]):int(st["cp_off"][j + 1])]
+                cu = su["copied"][int(su["cp_off"][j]):int(su["cp_off"][j + 1])]
+                assert c.tolist() == cu.tolist()
+                enc += (a1 - a0) + 4 * c.size
+        assert dense == hy["dense_sets"] and enc == hy["encoded_bytes"]
+    # no set above n/32: the hybrid run is the Huffman run
+    g = orc.assign_weights(random_graph(rng, 3000, 4000), "wc")
+    a, b = orc.run(g, 5, 0.5, 4, "hybrid", 3), orc.run(g, 5, 0.5, 4, "huffman", 3)
+    assert a["dense_sets"] == 0
+    skip = ("mode", "mode_override")  # hybrid is never the characterized mode
+    assert {k: v for k, v in a.items() if k not in skip} == {k: v for k, v in b.items() if k not in skip}

@@ -39,4 +39,4 @@ for r in range(a.reps):
     print(f"rep {r}: wall {wall:.2f}s theta {out['theta']} exit {out['exit_iteration']} est {out['estimation_samples']} "
           f"phases {out['phase_seconds']} ratio {out['compression_ratio']:.3f} store {out['device_store_bytes']/1e9:.2f} GB "
           f"edges {out['edges_scanned']:.3e} sample_ms {st['ms']:.0f} ({out['edges_scanned'] / (st['ms'] / 1e3) / 1e9:.1f} "
-          f"Gedges/s) seeds {out['seeds'][:6]} cov {out['coverage'][-1]:.5f} host {out['host_seconds']}", flush=True)
+          f"Gedges/s) seeds {out['seeds'][:6]} cov {out['coverage'][-1]:.5f} dense {out['dense_sets']} host {out['host_seconds']}", flush=True)
