@@ -39,7 +39,8 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
                            const uint8_t* __restrict__ code_len, int64_t top, uint32_t* __restrict__ bits,
                            uint64_t* __restrict__ nwords, uint64_t* __restrict__ ncopied, uint8_t* __restrict__ swap,
                            unsigned long long* __restrict__ payload, uint64_t dense_n, uint64_t base,
-                           uint32_t* __restrict__ dense_ids, unsigned long long* __restrict__ dense_cnt) {
+                           uint32_t* __restrict__ dense_ids, unsigned long long* __restrict__ dense_cnt,
+                           uint32_t* __restrict__ msize) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -47,6 +48,7 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
     for (uint64_t j = lo + w; j < hi; j += nw) {
         const uint64_t b = off[j];
         const uint32_t l = len[j];
+        if (lane == 0) msize[j - lo] = l;
         if (dense_n && 32ull * l > dense_n) {  // hybrid: an n-bit bitmap
             if (lane == 0) {
                 const uint64_t k = j - lo;
@@ -205,20 +207,48 @@ __device__ __forceinline__ bool decode_one(BitReader& br, const unsigned long lo
     }
 }
 
-// select_huffman round: thread per live set
-__global__ void k_huff_round(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
-                             const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
-                             const uint32_t* __restrict__ copied, uint64_t count, const unsigned long long* __restrict__ lut,
-                             uint32_t root_bits, const uint32_t* __restrict__ cover_pick, uint8_t* __restrict__ deleted,
-                             unsigned int* __restrict__ hist, unsigned long long* __restrict__ maxdec,
-                             unsigned long long* __restrict__ alg_bytes) {
-    const uint32_t pick = *cover_pick;
+// ---- select_huffman rounds (select.cpp:150-230) ------------------------------------
+// The reference decodes every live set per round: hits are deleted, misses recounted into a
+// fresh table.  The device splits a round in two passes with the same result:
+//   find  : decode each live set up to `pick` (no table writes); hits are deleted and listed,
+//           and the member volumes of hits (H) and misses (M) are summed;
+//   apply : the table over the live sets is either the old one minus the hits' members
+//           (cost H) or a recount of the misses (cost M): whichever is smaller runs.
+// Round 0 of a hub-dominated instance (config 2) covers giant sets: H >> M, so it recounts;
+// later rounds subtract a few hits.  Both give the reference's table exactly.
+enum : uint32_t { kApplyNone = 0, kApplySub = 1, kApplyRecount = 2 };
+
+struct RoundCtl {           // device control block of one select_huffman call
+    uint32_t pick;          // cover pick of the round (0xffffffff: padding round)
+    uint32_t padding;       // sticky: a gain-0 round stops further recounting
+    uint32_t apply;         // kApply*
+    uint32_t pad;
+    unsigned long long nhit;
+    unsigned long long vol[2];  // member volume of hits, misses
+};
+
+__device__ __forceinline__ void warp_add_u64(unsigned long long* p, unsigned long long x) {
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(p, x);
+}
+
+__global__ void k_huff_find(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
+                            const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
+                            const uint32_t* __restrict__ copied, const uint32_t* __restrict__ msize, uint64_t count,
+                            const unsigned long long* __restrict__ lut, uint32_t root_bits, RoundCtl* ctl,
+                            uint8_t* __restrict__ deleted, uint32_t* __restrict__ hitlist,
+                            unsigned long long* __restrict__ maxdec, unsigned long long* __restrict__ alg_bytes) {
+    const uint32_t pick = ctl->pick;
     if (pick == 0xffffffffu) return;
-    uint64_t local_max = 0, local_bytes = 0;
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < count; j += (uint64_t)gridDim.x * blockDim.x) {
-        if (deleted[j]) continue;
+    uint64_t local_max = 0;
+    unsigned long long hv = 0, mv = 0, by = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // all lanes iterate the same trip count (warp-level sums at the end)
+    for (uint64_t j0 = blockIdx.x * (uint64_t)blockDim.x; j0 < count; j0 += stride) {
+        const uint64_t j = j0 + threadIdx.x;
+        if (j >= count || deleted[j]) continue;
         const uint32_t nbits = bits[j];
-        if (nbits == kDenseBits) continue;  // hybrid bitmap sets: k_dense_round
+        if (nbits == kDenseBits) continue;  // hybrid bitmap sets: k_dense_find
         BitReader br;
         br.init(words + woff[j]);
         uint32_t pos = 0, nd = 0;
@@ -240,55 +270,147 @@ __global__ void k_huff_round(const uint32_t* __restrict__ words, const uint64_t*
                     break;
                 }
         local_max = nd > local_max ? nd : local_max;
-        const uint64_t payload = (nbits + 7) / 8 + 4 * (coff[j + 1] - coff[j]);
-        local_bytes += payload;
+        by += (nbits + 7) / 8 + 4 * (coff[j + 1] - coff[j]);
         if (found) {
-            local_bytes += payload;  // decoded again to subtract its members
             deleted[j] = 1;
-            // the set leaves the live collection: subtract all its members
-            br.init(words + woff[j]);
-            pos = 0;
-            while (pos < nbits) {
-                uint32_t sym, used;
-                if (!decode_one(br, lut, root_bits, sym, used)) break;
-                pos += used;
-                atomicSub(&hist[sym], 1u);
-            }
-            for (uint64_t c = coff[j]; c < coff[j + 1]; ++c) atomicSub(&hist[copied[c]], 1u);
+            hitlist[atomicAdd(&ctl->nhit, 1ull)] = (uint32_t)j;
+            hv += msize[j];
+        } else {
+            mv += msize[j];
         }
     }
-    if (local_max) atomicMax(maxdec, (unsigned long long)local_max);
-    if (local_bytes) atomicAdd(alg_bytes, (unsigned long long)local_bytes);
+    warp_add_u64(&ctl->vol[0], hv);
+    warp_add_u64(&ctl->vol[1], mv);
+    warp_add_u64(alg_bytes, by);
+    for (int o = 16; o; o >>= 1) local_max = max(local_max, (uint64_t)__shfl_xor_sync(FULL, local_max, o));
+    if ((threadIdx.x & 31) == 0 && local_max) atomicMax(maxdec, (unsigned long long)local_max);
 }
 
-// select round over the hybrid store's bitmap sets: CTA per set, test bit(pick); a covered
-// set subtracts every set bit (the same table the reference's recount of the misses gives)
-__global__ void k_dense_round(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
-                              const uint32_t* __restrict__ ids, uint64_t nd, uint64_t nwd,
-                              const uint32_t* __restrict__ cover_pick, uint8_t* __restrict__ deleted,
-                              unsigned int* __restrict__ hist, unsigned long long* __restrict__ alg_bytes) {
-    const uint32_t pick = *cover_pick;
+// hybrid bitmap sets, find pass: one thread per bitmap set (a bit test)
+__global__ void k_dense_find(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
+                             const uint32_t* __restrict__ ids, const uint32_t* __restrict__ msize, uint64_t nd,
+                             RoundCtl* ctl, uint8_t* __restrict__ deleted, uint32_t* __restrict__ dround, uint32_t r,
+                             unsigned long long* __restrict__ alg_bytes) {
+    const uint32_t pick = ctl->pick;
     if (pick == 0xffffffffu) return;
-    uint64_t local_bytes = 0;
+    unsigned long long hv = 0, mv = 0, by = 0;
+    for (uint64_t x0 = blockIdx.x * (uint64_t)blockDim.x; x0 < nd; x0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t x = x0 + threadIdx.x;
+        if (x >= nd) continue;
+        const uint32_t j = ids[x];
+        if (deleted[j]) continue;
+        by += 4;
+        if ((__ldg(words + woff[j] + (pick >> 5)) >> (pick & 31)) & 1u) {
+            deleted[j] = 1;
+            dround[x] = r + 1;
+            hv += msize[j];
+        } else {
+            mv += msize[j];
+        }
+    }
+    warp_add_u64(&ctl->vol[0], hv);
+    warp_add_u64(&ctl->vol[1], mv);
+    warp_add_u64(alg_bytes, by);
+}
+
+__global__ void k_round_decide(RoundCtl* ctl, uint64_t n) {
+    if (ctl->pick == 0xffffffffu) {
+        ctl->apply = kApplyNone;
+        return;
+    }
+    // recount = decode M members + clear n counters; subtract = decode H members
+    ctl->apply = ctl->vol[1] + n / 64 < ctl->vol[0] ? kApplyRecount : kApplySub;
+}
+
+__global__ void k_zero_if_recount(const RoundCtl* ctl, unsigned int* __restrict__ hist, uint64_t n) {
+    if (ctl->apply != kApplyRecount) return;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+        hist[v] = 0;
+}
+
+__device__ __forceinline__ void decode_all_add(const uint32_t* __restrict__ words, uint64_t wo, uint32_t nbits,
+                                               const uint32_t* __restrict__ copied, uint64_t c0, uint64_t c1,
+                                               const unsigned long long* __restrict__ lut, uint32_t root_bits,
+                                               unsigned int* __restrict__ hist, unsigned int delta) {
+    BitReader br;
+    br.init(words + wo);
+    uint32_t pos = 0;
+    while (pos < nbits) {
+        uint32_t sym, used;
+        if (!decode_one(br, lut, root_bits, sym, used)) break;
+        pos += used;
+        atomicAdd(&hist[sym], delta);
+    }
+    for (uint64_t c = c0; c < c1; ++c) atomicAdd(&hist[copied[c]], delta);
+}
+
+// apply pass, subtract: the hits of this round leave the table (delta = -1 mod 2^32)
+__global__ void k_huff_sub(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
+                           const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
+                           const uint32_t* __restrict__ copied, const unsigned long long* __restrict__ lut,
+                           uint32_t root_bits, const RoundCtl* ctl, const uint32_t* __restrict__ hitlist,
+                           unsigned int* __restrict__ hist, unsigned long long* __restrict__ alg_bytes) {
+    if (ctl->apply != kApplySub) return;
+    const uint64_t nh = ctl->nhit;
+    unsigned long long by = 0;
+    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < nh; i0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i0 + threadIdx.x;
+        if (i >= nh) continue;
+        const uint32_t j = hitlist[i];
+        const uint32_t nbits = bits[j];
+        if (nbits == kDenseBits) continue;
+        decode_all_add(words, woff[j], nbits, copied, coff[j], coff[j + 1], lut, root_bits, hist, 0xffffffffu);
+        by += (nbits + 7) / 8 + 4 * (coff[j + 1] - coff[j]);
+    }
+    warp_add_u64(alg_bytes, by);
+}
+
+// apply pass, recount: the table becomes the members of the live sets (select.cpp:196-199)
+__global__ void k_huff_recount(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
+                               const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
+                               const uint32_t* __restrict__ copied, uint64_t count,
+                               const unsigned long long* __restrict__ lut, uint32_t root_bits, const RoundCtl* ctl,
+                               const uint8_t* __restrict__ deleted, unsigned int* __restrict__ hist,
+                               unsigned long long* __restrict__ alg_bytes) {
+    if (ctl->apply != kApplyRecount) return;
+    unsigned long long by = 0;
+    for (uint64_t j0 = blockIdx.x * (uint64_t)blockDim.x; j0 < count; j0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = j0 + threadIdx.x;
+        if (j >= count || deleted[j]) continue;
+        const uint32_t nbits = bits[j];
+        if (nbits == kDenseBits) continue;
+        decode_all_add(words, woff[j], nbits, copied, coff[j], coff[j + 1], lut, root_bits, hist, 1u);
+        by += (nbits + 7) / 8 + 4 * (coff[j + 1] - coff[j]);
+    }
+    warp_add_u64(alg_bytes, by);
+}
+
+// hybrid bitmap sets, apply pass: CTA per bitmap set -- subtract this round's hits or
+// recount the live ones
+__global__ void k_dense_apply(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
+                              const uint32_t* __restrict__ ids, uint64_t nd, uint64_t nwd, const RoundCtl* ctl,
+                              const uint8_t* __restrict__ deleted, const uint32_t* __restrict__ dround, uint32_t r,
+                              unsigned int* __restrict__ hist, unsigned long long* __restrict__ alg_bytes) {
+    const uint32_t apply = ctl->apply;
+    if (apply == kApplyNone) return;
+    uint64_t by = 0;
     for (uint64_t x = blockIdx.x; x < nd; x += gridDim.x) {
         const uint32_t j = ids[x];
-        if (deleted[j]) continue;  // uniform over the CTA
+        const bool take = apply == kApplySub ? dround[x] == r + 1 : !deleted[j];
+        if (!take) continue;  // uniform over the CTA
+        const unsigned int delta = apply == kApplySub ? 0xffffffffu : 1u;
         const uint32_t* bm = words + woff[j];
-        local_bytes += 4;
-        if (!((__ldg(bm + (pick >> 5)) >> (pick & 31)) & 1u)) continue;
-        local_bytes += 4 * nwd;
+        by += 4 * nwd;
         for (uint64_t i = threadIdx.x; i < nwd; i += blockDim.x) {
             uint32_t m = __ldg(bm + i);
             while (m) {
                 const uint32_t b = __ffs(m) - 1;
                 m &= m - 1;
-                atomicSub(&hist[(uint32_t)(i * 32 + b)], 1u);
+                atomicAdd(&hist[(uint32_t)(i * 32 + b)], delta);
             }
         }
-        __syncthreads();
-        if (threadIdx.x == 0) deleted[j] = 1;
     }
-    if (threadIdx.x == 0 && local_bytes) atomicAdd(alg_bytes, (unsigned long long)local_bytes);
+    if (threadIdx.x == 0 && by) atomicAdd(alg_bytes, (unsigned long long)by);
 }
 
 // decode_find on one set with every reference corruption check (huffman.cpp:129-158)
@@ -332,22 +454,24 @@ __global__ void k_decode_find(const uint32_t* __restrict__ words, uint64_t woff,
 }
 
 __global__ void k_pick_from_key(const unsigned long long* __restrict__ keys, uint32_t r, uint8_t* __restrict__ is_seed,
-                                uint32_t* __restrict__ seeds, unsigned long long* __restrict__ marg,
-                                uint32_t* __restrict__ cover_pick, uint64_t n, uint32_t* __restrict__ padding) {
+                                uint32_t* __restrict__ seeds, unsigned long long* __restrict__ marg, RoundCtl* ctl,
+                                uint64_t n) {
     // padding persists: once a round had gain 0 the reference stops recounting (select.cpp:173-182)
     const unsigned long long key = keys[r];
     uint32_t pick = key ? 0xffffffffu - (uint32_t)(key & 0xffffffffu) : 0;
     uint32_t gain = (uint32_t)(key >> 32);
-    if (*padding) gain = 0;
+    if (ctl->padding) gain = 0;
     if (gain == 0) {
-        *padding = 1;
+        ctl->padding = 1;
         uint32_t p = 0;
         while (p < n && is_seed[p]) ++p;
         pick = p;
-        *cover_pick = 0xffffffffu;
+        ctl->pick = 0xffffffffu;
     } else {
-        *cover_pick = pick;
+        ctl->pick = pick;
     }
+    ctl->nhit = 0;
+    ctl->vol[0] = ctl->vol[1] = 0;
     is_seed[pick] = 1;
     seeds[r] = pick;
     marg[r] = gain;
@@ -400,6 +524,7 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     S.woff.reserve(base + cnt + 1, s);
     S.coff.reserve(base + cnt + 1, s);
     S.bits.reserve(base + cnt, s);
+    S.msize.reserve(base + cnt, s);
     DBuf<uint64_t> nwords, ncp;
     DBuf<uint8_t> swap;
     nwords.exact(cnt);
@@ -416,7 +541,8 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     }
     k_enc_size<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_len.p, top,
                                                    S.bits.p + base, nwords.p, ncp.p, swap.p, d_payload,
-                                                   S.hybrid ? S.n : 0, base, S.dense_ids.p, d_dense);
+                                                   S.hybrid ? S.n : 0, base, S.dense_ids.p, d_dense,
+                                                   S.msize.p + base);
     kt_size.stop();
     CK_LAUNCH("k_enc_size");
     d.kernel_launches++;
@@ -490,6 +616,7 @@ void store_append_host(Store& S, const uint8_t* bytes, uint64_t n_bytes, uint64_
     S.woff.reserve(base + 2, s);
     S.coff.reserve(base + 2, s);
     S.bits.reserve(base + 1, s);
+    S.msize.reserve(base + 1, s);
     S.words.reserve(S.total_words + nw + 4, s);
     S.copied.reserve(S.total_copied + n_cp + 1, s);
     std::vector<uint32_t> w(nw + 4, 0);
@@ -501,6 +628,9 @@ void store_append_host(Store& S, const uint8_t* bytes, uint64_t n_bytes, uint64_
     CK(cudaMemcpyAsync(S.woff.p + base + 1, &wo, 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(S.coff.p + base + 1, &co, 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(S.bits.p + base, &b32, 4, cudaMemcpyHostToDevice, s));
+    // member count unknown without decoding: an upper bound (it only steers select's apply pass)
+    const uint32_t msz = (uint32_t)std::min<uint64_t>(bit_length + n_cp, 0xffffffffULL);
+    CK(cudaMemcpyAsync(S.msize.p + base, &msz, 4, cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
     S.total_words = wo;
     S.total_copied = co;
@@ -562,30 +692,44 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
     mdec.exact(k);
     CK(cudaMemsetAsync(keys.p, 0, k * 8, s));
     CK(cudaMemsetAsync(mdec.p, 0, k * 8, s));
-    DBuf<uint32_t> seeds, ctl;
+    DBuf<uint32_t> seeds, hitlist, dround;
     seeds.exact(k);
-    ctl.exact(2);  // [0] cover pick, [1] padding flag
-    CK(cudaMemsetAsync(ctl.p, 0, 8, s));
+    hitlist.exact(theta);
+    dround.exact(std::max<uint64_t>(S.dense_count, 1));
+    CK(cudaMemsetAsync(dround.p, 0, std::max<uint64_t>(S.dense_count, 1) * 4, s));
+    DBuf<unsigned long long> ctlbuf;
+    ctlbuf.exact((sizeof(RoundCtl) + 7) / 8);
+    RoundCtl* ctl = reinterpret_cast<RoundCtl*>(ctlbuf.p);
+    CK(cudaMemsetAsync(ctl, 0, sizeof(RoundCtl), s));
     const unsigned grid = grid_for(theta, d);
+    const unsigned grid_n = grid_for(n, d);
+    const uint64_t nd = S.dense_count, nwd = (n + 31) / 32;
     DBuf<unsigned long long> rbytes;
     rbytes.exact(k);
     CK(cudaMemsetAsync(rbytes.p, 0, k * 8, s));
     std::vector<KTimer> kt(k);
     for (uint32_t r = 0; r < k; ++r) {
         argmax_dev(d, d_hist, n, keys.p + r);
-        k_pick_from_key<<<1, 1, 0, s>>>(keys.p, r, is_seed.p, seeds.p, marg.p, ctl.p, n, ctl.p + 1);
+        k_pick_from_key<<<1, 1, 0, s>>>(keys.p, r, is_seed.p, seeds.p, marg.p, ctl, n);
         kt[r].start(&d, IMMX_KSTAT_HSELECT);
-        k_huff_round<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, theta, S.lut.p,
-                                         S.lut_root_bits, ctl.p, deleted.p, d_hist, mdec.p + r, rbytes.p + r);
-        if (S.dense_count) {
-            k_dense_round<<<(unsigned)std::min<uint64_t>(S.dense_count, (uint64_t)d.num_sms * 8), 256, 0, s>>>(
-                S.words.p, S.woff.p, S.dense_ids.p, S.dense_count, (n + 31) / 32, ctl.p, deleted.p, d_hist,
-                rbytes.p + r);
-            d.kernel_launches++;
-        }
+        k_huff_find<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, S.msize.p, theta,
+                                         S.lut.p, S.lut_root_bits, ctl, deleted.p, hitlist.p, mdec.p + r,
+                                         rbytes.p + r);
+        if (nd)
+            k_dense_find<<<grid_for(nd, d), 256, 0, s>>>(S.words.p, S.woff.p, S.dense_ids.p, S.msize.p, nd, ctl,
+                                                         deleted.p, dround.p, r, rbytes.p + r);
+        k_round_decide<<<1, 1, 0, s>>>(ctl, n);
+        k_zero_if_recount<<<grid_n, 256, 0, s>>>(ctl, d_hist, n);
+        k_huff_sub<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, S.lut.p,
+                                        S.lut_root_bits, ctl, hitlist.p, d_hist, rbytes.p + r);
+        k_huff_recount<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, theta, S.lut.p,
+                                            S.lut_root_bits, ctl, deleted.p, d_hist, rbytes.p + r);
+        if (nd)
+            k_dense_apply<<<(unsigned)std::min<uint64_t>(nd, (uint64_t)d.num_sms * 8), 256, 0, s>>>(
+                S.words.p, S.woff.p, S.dense_ids.p, nd, nwd, ctl, deleted.p, dround.p, r, d_hist, rbytes.p + r);
         kt[r].stop();
         CK_LAUNCH("select_huffman round");
-        d.kernel_launches += 2;
+        d.kernel_launches += 6 + (nd ? 2 : 0);
     }
     std::vector<unsigned long long> hbytes(k);
     CK(cudaMemcpyAsync(hbytes.data(), rbytes.p, k * 8, cudaMemcpyDeviceToHost, s));

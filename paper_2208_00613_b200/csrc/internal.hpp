@@ -165,6 +165,7 @@ struct Store {
     uint64_t count = 0;
     DBuf<uint64_t> woff;   // count+1 word offsets
     DBuf<uint32_t> bits;   // count
+    DBuf<uint32_t> msize;  // count: members per set (steers select's apply pass)
     DBuf<uint64_t> coff;   // count+1
     DBuf<uint32_t> words;
     DBuf<uint32_t> copied;
