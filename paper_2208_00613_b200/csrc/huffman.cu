@@ -232,6 +232,137 @@ __device__ __forceinline__ void warp_add_u64(unsigned long long* p, unsigned lon
     if ((threadIdx.x & 31) == 0 && x) atomicAdd(p, x);
 }
 
+// r-th (0-based) set bit of x (popc(x) > r)
+__device__ __forceinline__ uint32_t nth_set_bit(uint32_t x, uint32_t r) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (int w = 16; w; w >>= 1) {
+        const uint32_t c = __popc(x & ((1u << w) - 1u));
+        if (r >= c) {
+            r -= c;
+            x >>= w;
+            pos += w;
+        }
+    }
+    return pos;
+}
+
+// Warp-cooperative decode over the sets of a range: every lane holds one set and decodes one
+// codeword per step; lanes whose set ended take the next live sets of the warp's range (a
+// ballot over 32 candidates, handed out in order) once a quarter of the warp is idle, so the
+// lanes stay busy whatever the set sizes (thread-per-set decode ran ~3 of 32 lanes on c4).
+// Op: bool live(i, j&) -- index i of the range -> set j, false to skip;
+//     bool sym(j, v)   -- a decoded codeword, true stops this set;
+//     void end(j, stopped, ncodewords, nbits) -- the set is done.
+template <class Op>
+__device__ __forceinline__ void warp_decode_range(uint64_t lo, uint64_t hi, const uint32_t* __restrict__ words,
+                                                  const uint64_t* __restrict__ woff,
+                                                  const uint32_t* __restrict__ bits,
+                                                  const unsigned long long* __restrict__ lut, uint32_t root_bits,
+                                                  Op& op) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint64_t cur = lo;
+    bool active = false, fresh = false;
+    uint32_t j = 0, pos = 0, nbits = 0, nd = 0;
+    BitReader br;
+    for (;;) {
+        uint32_t idle = __ballot_sync(FULL, !active);
+        if (idle && cur < hi && (__popc(idle) >= 8 || idle == FULL)) {
+            do {  // refill the idle lanes in range order
+                const uint64_t i = cur + lane;
+                uint32_t jj = 0;
+                const bool lv = i < hi && op.live(i, jj);
+                const uint32_t L = __ballot_sync(FULL, lv);
+                const uint32_t take = min(__popc(L), __popc(idle));
+                const uint32_t r = __popc(idle & lt);
+                const bool assign = !active && r < take;
+                const uint32_t src = assign ? nth_set_bit(L, r) : lane;
+                const uint32_t jsrc = __shfl_sync(FULL, jj, src);
+                if (assign) {
+                    j = jsrc;
+                    active = fresh = true;
+                }
+                const uint64_t adv = take < (uint32_t)__popc(L) ? nth_set_bit(L, take) : 32;
+                cur += adv;
+                idle = __ballot_sync(FULL, !active);
+            } while (idle && cur < hi);
+        }
+        if (!__any_sync(FULL, active)) break;
+        if (fresh) {  // newly assigned: open the stream
+            nbits = bits[j];
+            br.init(words + woff[j]);
+            pos = 0;
+            nd = 0;
+            fresh = false;
+        }
+        if (active) {
+            bool stop = false;
+            if (pos < nbits) {
+                uint32_t sym, used;
+                if (decode_one(br, lut, root_bits, sym, used)) {
+                    pos += used;
+                    nd++;
+                    stop = op.sym(j, sym);
+                } else {
+                    pos = nbits;  // cannot happen on our own streams
+                }
+            }
+            if (stop || pos >= nbits) {
+                op.end(j, stop, nd, nbits);
+                active = false;
+            }
+        }
+    }
+}
+
+struct FindOp {
+    const uint8_t* deleted;
+    const uint32_t* bits;
+    const uint64_t* coff;
+    const uint32_t* copied;
+    const uint32_t* msize;
+    uint8_t* deleted_w;
+    uint32_t* hitlist;
+    RoundCtl* ctl;
+    uint32_t pick;
+    uint64_t maxd = 0;
+    unsigned long long hv = 0, mv = 0, by = 0;
+    __device__ bool live(uint64_t i, uint32_t& j) {
+        j = (uint32_t)i;
+        return !deleted[i] && bits[i] != kDenseBits;
+    }
+    __device__ bool sym(uint32_t, uint32_t v) { return v == pick; }
+    __device__ void end(uint32_t j, bool stopped, uint32_t nd, uint32_t nbits) {
+        bool found = stopped;
+        const uint64_t c0 = coff[j], c1 = coff[j + 1];
+        if (!found)
+            for (uint64_t c = c0; c < c1; ++c)
+                if (copied[c] == pick) {
+                    found = true;
+                    break;
+                }
+        maxd = nd > maxd ? nd : maxd;
+        by += (nbits + 7) / 8 + 4 * (c1 - c0);
+        if (found) {
+            deleted_w[j] = 1;
+            hitlist[atomicAdd(&ctl->nhit, 1ull)] = j;
+            hv += msize[j];
+        } else {
+            mv += msize[j];
+        }
+    }
+};
+
+// the warp's share of [0, count): contiguous ranges, one per warp of the grid
+__device__ __forceinline__ void warp_range(uint64_t count, uint64_t& lo, uint64_t& hi) {
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t per = (count + nw - 1) / nw;
+    lo = min(count, w * per);
+    hi = min(count, lo + per);
+}
+
 __global__ void k_huff_find(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
                             const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
                             const uint32_t* __restrict__ copied, const uint32_t* __restrict__ msize, uint64_t count,
@@ -240,48 +371,14 @@ __global__ void k_huff_find(const uint32_t* __restrict__ words, const uint64_t* 
                             unsigned long long* __restrict__ maxdec, unsigned long long* __restrict__ alg_bytes) {
     const uint32_t pick = ctl->pick;
     if (pick == 0xffffffffu) return;
-    uint64_t local_max = 0;
-    unsigned long long hv = 0, mv = 0, by = 0;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    // all lanes iterate the same trip count (warp-level sums at the end)
-    for (uint64_t j0 = blockIdx.x * (uint64_t)blockDim.x; j0 < count; j0 += stride) {
-        const uint64_t j = j0 + threadIdx.x;
-        if (j >= count || deleted[j]) continue;
-        const uint32_t nbits = bits[j];
-        if (nbits == kDenseBits) continue;  // hybrid bitmap sets: k_dense_find
-        BitReader br;
-        br.init(words + woff[j]);
-        uint32_t pos = 0, nd = 0;
-        bool found = false;
-        while (pos < nbits) {
-            uint32_t sym, used;
-            if (!decode_one(br, lut, root_bits, sym, used)) break;  // cannot happen on our own streams
-            pos += used;
-            nd++;
-            if (sym == pick) {
-                found = true;
-                break;
-            }
-        }
-        if (!found)
-            for (uint64_t c = coff[j]; c < coff[j + 1]; ++c)
-                if (copied[c] == pick) {
-                    found = true;
-                    break;
-                }
-        local_max = nd > local_max ? nd : local_max;
-        by += (nbits + 7) / 8 + 4 * (coff[j + 1] - coff[j]);
-        if (found) {
-            deleted[j] = 1;
-            hitlist[atomicAdd(&ctl->nhit, 1ull)] = (uint32_t)j;
-            hv += msize[j];
-        } else {
-            mv += msize[j];
-        }
-    }
-    warp_add_u64(&ctl->vol[0], hv);
-    warp_add_u64(&ctl->vol[1], mv);
-    warp_add_u64(alg_bytes, by);
+    FindOp op{deleted, bits, coff, copied, msize, deleted, hitlist, ctl, pick};
+    uint64_t lo, hi;
+    warp_range(count, lo, hi);
+    warp_decode_range(lo, hi, words, woff, bits, lut, root_bits, op);
+    warp_add_u64(&ctl->vol[0], op.hv);
+    warp_add_u64(&ctl->vol[1], op.mv);
+    warp_add_u64(alg_bytes, op.by);
+    uint64_t local_max = op.maxd;
     for (int o = 16; o; o >>= 1) local_max = max(local_max, (uint64_t)__shfl_xor_sync(FULL, local_max, o));
     if ((threadIdx.x & 31) == 0 && local_max) atomicMax(maxdec, (unsigned long long)local_max);
 }
@@ -328,44 +425,45 @@ __global__ void k_zero_if_recount(const RoundCtl* ctl, unsigned int* __restrict_
         hist[v] = 0;
 }
 
-__device__ __forceinline__ void decode_all_add(const uint32_t* __restrict__ words, uint64_t wo, uint32_t nbits,
-                                               const uint32_t* __restrict__ copied, uint64_t c0, uint64_t c1,
-                                               const unsigned long long* __restrict__ lut, uint32_t root_bits,
-                                               unsigned int* __restrict__ hist, unsigned int delta) {
-    BitReader br;
-    br.init(words + wo);
-    uint32_t pos = 0;
-    while (pos < nbits) {
-        uint32_t sym, used;
-        if (!decode_one(br, lut, root_bits, sym, used)) break;
-        pos += used;
-        atomicAdd(&hist[sym], delta);
+// apply pass: add `delta` for every member of the listed (subtract: this round's hits,
+// delta = -1 mod 2^32) or live (recount: select.cpp:196-199, delta = +1) sets
+struct ApplyOp {
+    const uint8_t* deleted;     // recount: live = !deleted
+    const uint32_t* hitlist;    // subtract: the round's hits
+    const uint32_t* bits;
+    const uint64_t* coff;
+    const uint32_t* copied;
+    unsigned int* hist;
+    unsigned int delta;
+    unsigned long long by = 0;
+    __device__ bool live(uint64_t i, uint32_t& j) {
+        j = hitlist ? hitlist[i] : (uint32_t)i;
+        return (hitlist || !deleted[i]) && bits[j] != kDenseBits;
     }
-    for (uint64_t c = c0; c < c1; ++c) atomicAdd(&hist[copied[c]], delta);
-}
+    __device__ bool sym(uint32_t, uint32_t v) {
+        atomicAdd(&hist[v], delta);
+        return false;
+    }
+    __device__ void end(uint32_t j, bool, uint32_t, uint32_t nbits) {
+        const uint64_t c0 = coff[j], c1 = coff[j + 1];
+        for (uint64_t c = c0; c < c1; ++c) atomicAdd(&hist[copied[c]], delta);
+        by += (nbits + 7) / 8 + 4 * (c1 - c0);
+    }
+};
 
-// apply pass, subtract: the hits of this round leave the table (delta = -1 mod 2^32)
 __global__ void k_huff_sub(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
                            const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
                            const uint32_t* __restrict__ copied, const unsigned long long* __restrict__ lut,
                            uint32_t root_bits, const RoundCtl* ctl, const uint32_t* __restrict__ hitlist,
                            unsigned int* __restrict__ hist, unsigned long long* __restrict__ alg_bytes) {
     if (ctl->apply != kApplySub) return;
-    const uint64_t nh = ctl->nhit;
-    unsigned long long by = 0;
-    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < nh; i0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = i0 + threadIdx.x;
-        if (i >= nh) continue;
-        const uint32_t j = hitlist[i];
-        const uint32_t nbits = bits[j];
-        if (nbits == kDenseBits) continue;
-        decode_all_add(words, woff[j], nbits, copied, coff[j], coff[j + 1], lut, root_bits, hist, 0xffffffffu);
-        by += (nbits + 7) / 8 + 4 * (coff[j + 1] - coff[j]);
-    }
-    warp_add_u64(alg_bytes, by);
+    ApplyOp op{nullptr, hitlist, bits, coff, copied, hist, 0xffffffffu};
+    uint64_t lo, hi;
+    warp_range(ctl->nhit, lo, hi);
+    warp_decode_range(lo, hi, words, woff, bits, lut, root_bits, op);
+    warp_add_u64(alg_bytes, op.by);
 }
 
-// apply pass, recount: the table becomes the members of the live sets (select.cpp:196-199)
 __global__ void k_huff_recount(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
                                const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
                                const uint32_t* __restrict__ copied, uint64_t count,
@@ -373,16 +471,11 @@ __global__ void k_huff_recount(const uint32_t* __restrict__ words, const uint64_
                                const uint8_t* __restrict__ deleted, unsigned int* __restrict__ hist,
                                unsigned long long* __restrict__ alg_bytes) {
     if (ctl->apply != kApplyRecount) return;
-    unsigned long long by = 0;
-    for (uint64_t j0 = blockIdx.x * (uint64_t)blockDim.x; j0 < count; j0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t j = j0 + threadIdx.x;
-        if (j >= count || deleted[j]) continue;
-        const uint32_t nbits = bits[j];
-        if (nbits == kDenseBits) continue;
-        decode_all_add(words, woff[j], nbits, copied, coff[j], coff[j + 1], lut, root_bits, hist, 1u);
-        by += (nbits + 7) / 8 + 4 * (coff[j + 1] - coff[j]);
-    }
-    warp_add_u64(alg_bytes, by);
+    ApplyOp op{deleted, nullptr, bits, coff, copied, hist, 1u};
+    uint64_t lo, hi;
+    warp_range(count, lo, hi);
+    warp_decode_range(lo, hi, words, woff, bits, lut, root_bits, op);
+    warp_add_u64(alg_bytes, op.by);
 }
 
 // hybrid bitmap sets, apply pass: CTA per bitmap set -- subtract this round's hits or
