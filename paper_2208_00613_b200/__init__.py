@@ -29,6 +29,8 @@ __all__ = [
     "load_edge_list", "load_edge_list_text", "load_graph_cache", "merged_argmax", "run", "sample_block",
     "sample_rrr", "save_graph_cache", "select_raw", "skewness", "table_argmax", "theta_bound",
     "theta_bound_real", "transpose",
+    # the C++ API's stats output (pipeline.hpp:66-71)
+    "stats_to_json", "write_stats", "write_seeds",
     # B200 additions
     "Device", "default_device", "generate_rmat", "generate_er", "DeviceGraph", "Pool", "run_device",
 ]
@@ -809,3 +811,39 @@ def run(graph: Graph, k: int, *, epsilon=0.5, blocks=8, mode="auto", seed=42, wo
     }
     return {"seeds": r["seeds"], "marginal": r["marginal"], "coverage": r["coverage"], "padded": r["padded"],
             "seed_ids": [int(ids[s]) for s in r["seeds"]], "stats": stats}
+
+
+# ----------------------------------------------------------------------------- stats output
+_STATS_KEYS = ("n", "m", "theta", "skewness", "density", "mode", "mode_override", "phase_seconds", "raw_bytes",
+               "encoded_bytes", "compression_ratio", "peak_bytes", "padded_seeds", "uncoded_vertex_fraction",
+               "blocks", "seeds", "plan", "original_ids", "rss_bytes")
+
+
+def stats_to_json(stats: dict) -> str:
+    """stats_json.cpp:21-72: the run stats (the dict ``run`` returns) in the reference's schema
+    and key order, 2-space indented.  The device-only counters (``stats["device"]``) are not
+    part of that schema and are left out."""
+    import json
+
+    out = {key: stats[key] for key in _STATS_KEYS}
+    out["rss_bytes"] = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss * 1024  # informational
+    return json.dumps(out, indent=2)
+
+
+def write_stats(stats: dict, path: str) -> None:
+    """stats_json.cpp:74-79"""
+    try:
+        with open(path, "w") as f:
+            f.write(stats_to_json(stats) + "\n")
+    except OSError as e:
+        raise RuntimeError(f"cannot write stats to '{path}'") from e
+
+
+def write_seeds(stats: dict, path: str) -> None:
+    """stats_json.cpp:81-86: one original vertex id per line"""
+    try:
+        with open(path, "w") as f:
+            for s in stats["seeds"]:
+                f.write(f"{s['id']}\n")
+    except OSError as e:
+        raise RuntimeError(f"cannot write seeds to '{path}'") from e
