@@ -703,7 +703,7 @@ int immx_store_info(const immx_store* s, uint64_t* count, uint64_t* payload, uin
         if (count) *count = s->s.count;
         if (payload) *payload = s->s.payload_bytes;
         if (device_bytes)
-            *device_bytes = s->s.total_words * 4 + s->s.total_copied * 4 + (s->s.count + 1) * 16 + s->s.count * 4;
+            *device_bytes = s->s.device_bytes();
     });
 }
 int immx_store_read(const immx_store* s, uint64_t lo, uint64_t hi, uint64_t* byte_off, uint8_t* bytes,
@@ -926,6 +926,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     store = d.run_store;
                     store->s.count = store->s.total_words = store->s.total_copied = store->s.payload_bytes = 0;
                     store->s.dense_count = 0;
+                    store->s.n_extra = 0;
                     store->s.hybrid = mode == IMMX_MODE_HYBRID;
                     store_set_codes(store->s, d, n, cb.bits.data(), cb.len.data(), lut, rb);
                 } else if (mode == IMMX_MODE_BITMAP) {
@@ -1006,7 +1007,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         uint64_t store_dev_bytes = 0;
         if (store) {
             const Store& S = store->s;
-            store_dev_bytes = S.total_words * 4 + S.total_copied * 4 + (S.count + 1) * 16 + S.count * 4;
+            store_dev_bytes = S.device_bytes();
         } else if (bm) {
             store_dev_bytes = n * bm->b.total_wpr() * 4;
         } else {

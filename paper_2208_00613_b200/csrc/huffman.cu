@@ -16,6 +16,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.hpp"
@@ -40,7 +42,7 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
                            uint64_t* __restrict__ nwords, uint64_t* __restrict__ ncopied, uint8_t* __restrict__ swap,
                            unsigned long long* __restrict__ payload, uint64_t dense_n, uint64_t base,
                            uint32_t* __restrict__ dense_ids, unsigned long long* __restrict__ dense_cnt,
-                           uint32_t* __restrict__ msize) {
+                           uint32_t* __restrict__ msize, uint32_t* __restrict__ ncw, uint64_t* __restrict__ nx) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -57,6 +59,8 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
                 nwords[k] = nwd;
                 ncopied[k] = 0;
                 swap[k] = 0;
+                ncw[k] = 0;
+                nx[k] = 0;
                 atomicAdd(payload, (unsigned long long)(4 * nwd));
                 dense_ids[atomicAdd(dense_cnt, 1ull)] = (uint32_t)(base + k);
             }
@@ -82,6 +86,9 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
             nwords[k] = (nb + 31) / 32;
             ncopied[k] = nc;
             swap[k] = has_top;
+            const uint32_t cw = l - nc;
+            ncw[k] = cw;
+            nx[k] = cw > kSegCodewords ? (cw - 1) / kSegCodewords : 0;
             atomicAdd(payload, (unsigned long long)((nb + 7) / 8 + 4ull * nc));
         }
     }
@@ -105,7 +112,9 @@ __global__ void k_enc_pack(const uint32_t* __restrict__ arena, const uint64_t* _
                            const uint64_t* __restrict__ code_bits, const uint8_t* __restrict__ code_len, int64_t top,
                            const uint8_t* __restrict__ swap, const uint64_t* __restrict__ woff,
                            const uint64_t* __restrict__ coff, uint32_t* __restrict__ words,
-                           uint32_t* __restrict__ copied, const uint32_t* __restrict__ bits) {
+                           uint32_t* __restrict__ copied, const uint32_t* __restrict__ bits,
+                           const uint64_t* __restrict__ xoff, uint64_t base, uint32_t* __restrict__ xset,
+                           uint32_t* __restrict__ xbit) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t lt = lanemask_lt();
     const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -125,10 +134,12 @@ __global__ void k_enc_pack(const uint32_t* __restrict__ arena, const uint64_t* _
         uint32_t* cp = copied + coff[k];
         const bool sw = swap[k];
         uint64_t bitpos = 0;
-        uint32_t ncp = 0;
+        uint32_t ncp = 0, ncw = 0;  // codewords so far (the stream order: top first)
+        const uint64_t x0 = xoff[k];
         if (sw) {
             if (lane == 0) put_code(out, 0, code_bits[top], code_len[top]);
             bitpos = code_len[top];
+            ncw = 1;
         }
         for (uint32_t i0 = 0; i0 < l; i0 += 32) {
             const uint32_t i = i0 + lane;
@@ -150,6 +161,17 @@ __global__ void k_enc_pack(const uint32_t* __restrict__ arena, const uint64_t* _
             const uint32_t um = __ballot_sync(FULL, unc);
             if (unc) cp[ncp + __popc(um & lt)] = v;
             ncp += __popc(um);
+            // checkpoint: codeword number c (c % kSegCodewords == 0, c > 0) starts a segment
+            const uint32_t cm = __ballot_sync(FULL, L != 0);
+            if (L) {
+                const uint32_t c = ncw + __popc(cm & lt);
+                if (c && c % kSegCodewords == 0) {
+                    const uint64_t xi = x0 + c / kSegCodewords - 1;
+                    xset[xi] = (uint32_t)(base + k);
+                    xbit[xi] = (uint32_t)(bitpos + x - L);
+                }
+            }
+            ncw += __popc(cm);
             bitpos += __shfl_sync(FULL, x, 31);
         }
     }
@@ -210,21 +232,32 @@ __device__ __forceinline__ bool decode_one(BitReader& br, const unsigned long lo
 // ---- select_huffman rounds (select.cpp:150-230) ------------------------------------
 // The reference decodes every live set per round: hits are deleted, misses recounted into a
 // fresh table.  The device splits a round in two passes with the same result:
-//   find  : decode each live set up to `pick` (no table writes); hits are deleted and listed,
-//           and the member volumes of hits (H) and misses (M) are summed;
+//   find  : decode each live set up to `pick` (no table writes); hits are deleted (marked
+//           with the round) and listed, and the member volume of the hits (H) is summed;
 //   apply : the table over the live sets is either the old one minus the hits' members
-//           (cost H) or a recount of the misses (cost M): whichever is smaller runs.
+//           (cost H) or a recount of the misses (cost M = live volume - H) into the other,
+//           pre-cleared table: whichever is smaller runs.
 // Round 0 of a hub-dominated instance (config 2) covers giant sets: H >> M, so it recounts;
 // later rounds subtract a few hits.  Both give the reference's table exactly.
+// Work items are decode segments: segment 0 of every set (items [0, theta)) and the extra
+// segments of sets longer than kSegCodewords codewords (items theta + x), each starting at a
+// checkpoint the encoder recorded, so one large set is decoded by many lanes at once.
 enum : uint32_t { kApplyNone = 0, kApplySub = 1, kApplyRecount = 2 };
 
 struct RoundCtl {           // device control block of one select_huffman call
     uint32_t pick;          // cover pick of the round (0xffffffff: padding round)
     uint32_t padding;       // sticky: a gain-0 round stops further recounting
-    uint32_t apply;         // kApply*
-    uint32_t pad;
+    uint32_t apply;         // kApply* of the round (written by the apply pass)
+    uint32_t cur;           // live table: hist[cur] (a recount fills the other one)
+    uint32_t cur_snap;      // cur as the round's find pass saw it
+    uint32_t done;          // blocks of the argmax pass that finished
     unsigned long long nhit;
-    unsigned long long vol[2];  // member volume of hits, misses
+    unsigned long long hvol;      // member volume of this round's hits
+    unsigned long long live_vol;  // member volume of the live sets (before this round)
+    unsigned long long live_snap; // live_vol as the round's find pass saw it
+    unsigned long long queue[2];  // work queues of the find and apply passes
+    unsigned long long nlist[2];  // item lists: the items the round's find pass took
+    unsigned long long nhitx;     // extra segments of this round's hits
 };
 
 __device__ __forceinline__ void warp_add_u64(unsigned long long* p, unsigned long long x) {
@@ -247,136 +280,225 @@ __device__ __forceinline__ uint32_t nth_set_bit(uint32_t x, uint32_t r) {
     return pos;
 }
 
-// Warp-cooperative decode over the sets of a range: every lane holds one set and decodes one
-// codeword per step; lanes whose set ended take the next live sets of the warp's range (a
-// ballot over 32 candidates, handed out in order) once a quarter of the warp is idle, so the
-// lanes stay busy whatever the set sizes (thread-per-set decode ran ~3 of 32 lanes on c4).
-// Op: bool live(i, j&) -- index i of the range -> set j, false to skip;
-//     bool sym(j, v)   -- a decoded codeword, true stops this set;
-//     void end(j, stopped, ncodewords, nbits) -- the set is done.
-template <class Op>
-__device__ __forceinline__ void warp_decode_range(uint64_t lo, uint64_t hi, const uint32_t* __restrict__ words,
-                                                  const uint64_t* __restrict__ woff,
-                                                  const uint32_t* __restrict__ bits,
+struct SegView {  // the store's segment index
+    const uint32_t* words;
+    const uint64_t* woff;
+    const uint32_t* bits;
+    const uint8_t* segd;
+    const uint32_t* xset;
+    const uint32_t* xbit;
+    const uint32_t* xfirst;
+    uint64_t count;
+    __device__ uint32_t set_of(uint64_t i) const { return i < count ? (uint32_t)i : xset[i - count]; }
+};
+
+// Warp-cooperative decode over work items [0, total): every lane holds one segment and
+// decodes one codeword per step; lanes whose segment ended take the next live items (a
+// ballot over 32 candidates, handed out in order) once a quarter of the warp is idle, and the
+// warp takes chunks of items from a global queue, so lanes stay busy whatever the set sizes.
+// Op: bool live(j)                 -- set j takes part in this pass;
+//     bool sym(have, v, idx)       -- called by the whole warp each step (have: a codeword
+//                                     v with index idx in its set was decoded); true stops
+//     void end(j, seg0, stopped, idx_last, nbits) -- a segment is done (idx_last = index of
+//                                     its last decoded codeword + 1).
+// item sources: all items; a list of items; the hits of the round (their segment 0s, then
+// their extra segments)
+struct RangeSrc {
+    __device__ uint32_t at(uint64_t i) const { return (uint32_t)i; }
+};
+struct ListSrc {
+    const uint32_t* l;
+    __device__ uint32_t at(uint64_t i) const { return l[i]; }
+};
+struct HitSrc {
+    const uint32_t* hits;
+    const uint32_t* hitx;
+    uint64_t nhit, count;
+    __device__ uint32_t at(uint64_t i) const { return i < nhit ? hits[i] : (uint32_t)(count + hitx[i - nhit]); }
+};
+
+template <class Src, class Op>
+__device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict__ queue, const Src& srcs,
+                                                  uint64_t total, const SegView& sv,
                                                   const unsigned long long* __restrict__ lut, uint32_t root_bits,
-                                                  Op& op) {
+                                                  Op& op, uint32_t* __restrict__ out_list = nullptr,
+                                                  unsigned long long* __restrict__ out_cnt = nullptr) {
+    // chunks of up to 64 items, fewer when the pass is small (every warp should get work)
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t kChunk = (uint32_t)max((uint64_t)1, min((uint64_t)64, total / (nwarps * 2)));
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    uint64_t cur = lo;
+    uint64_t cur = 0, hi = 0;
+    bool drained = false;
     bool active = false, fresh = false;
-    uint32_t j = 0, pos = 0, nbits = 0, nd = 0;
+    uint32_t j = 0, pos = 0, nbits = 0, nd = 0, base = 0, lim = 0xffffffffu;
+    bool seg0 = false;
+    uint64_t item = 0;
     BitReader br;
     for (;;) {
         uint32_t idle = __ballot_sync(FULL, !active);
-        if (idle && cur < hi && (__popc(idle) >= 8 || idle == FULL)) {
-            do {  // refill the idle lanes in range order
+        if (idle && !drained && (__popc(idle) >= 8 || idle == FULL)) {
+            do {  // refill the idle lanes in item order
+                if (cur >= hi) {
+                    unsigned long long b0 = 0;
+                    if (lane == 0) b0 = atomicAdd(queue, (unsigned long long)kChunk);
+                    b0 = __shfl_sync(FULL, b0, 0);
+                    if (b0 >= total) {
+                        drained = true;
+                        break;
+                    }
+                    cur = b0;
+                    hi = min((unsigned long long)total, b0 + kChunk);
+                }
                 const uint64_t i = cur + lane;
-                uint32_t jj = 0;
-                const bool lv = i < hi && op.live(i, jj);
+                const uint32_t it = i < hi ? srcs.at(i) : 0u;
+                const bool lv = i < hi && op.live(sv.set_of(it));
                 const uint32_t L = __ballot_sync(FULL, lv);
                 const uint32_t take = min(__popc(L), __popc(idle));
                 const uint32_t r = __popc(idle & lt);
                 const bool assign = !active && r < take;
                 const uint32_t src = assign ? nth_set_bit(L, r) : lane;
-                const uint32_t jsrc = __shfl_sync(FULL, jj, src);
+                const uint32_t isrc = __shfl_sync(FULL, it, src);
                 if (assign) {
-                    j = jsrc;
+                    item = isrc;
                     active = fresh = true;
                 }
-                const uint64_t adv = take < (uint32_t)__popc(L) ? nth_set_bit(L, take) : 32;
-                cur += adv;
+                if (out_list) {  // the taken items are the next round's candidates
+                    const uint32_t A = __ballot_sync(FULL, assign);
+                    unsigned long long ob = 0;
+                    if (lane == 0 && A) ob = atomicAdd(out_cnt, (unsigned long long)__popc(A));
+                    ob = __shfl_sync(FULL, ob, 0);
+                    if (assign) out_list[ob + __popc(A & lt)] = isrc;
+                }
+                cur += take < (uint32_t)__popc(L) ? nth_set_bit(L, take) : 32;
                 idle = __ballot_sync(FULL, !active);
-            } while (idle && cur < hi);
+            } while (idle);
         }
-        if (!__any_sync(FULL, active)) break;
-        if (fresh) {  // newly assigned: open the stream
-            nbits = bits[j];
-            br.init(words + woff[j]);
-            pos = 0;
+        if (!__any_sync(FULL, active)) {
+            if (drained) break;
+            continue;
+        }
+        if (fresh) {  // newly assigned: open the segment
+            uint32_t bit0 = 0;
+            if (item < sv.count) {
+                j = (uint32_t)item;
+                seg0 = true;
+                base = 0;
+                lim = sv.segd[j] ? kSegCodewords : 0xffffffffu;
+            } else {
+                const uint64_t x = item - sv.count;
+                j = sv.xset[x];
+                seg0 = false;
+                bit0 = sv.xbit[x];
+                base = (uint32_t)(x - sv.xfirst[j] + 1) * kSegCodewords;
+                lim = kSegCodewords;
+            }
+            nbits = sv.bits[j];
+            if (nbits == kDenseBits) nbits = 0;  // hybrid bitmap sets: the k_dense_* passes
+            br.init(sv.words + sv.woff[j] + (bit0 >> 5));
+            if (bit0 & 31) br.skip(bit0 & 31);
+            pos = bit0;
             nd = 0;
             fresh = false;
         }
-        if (active) {
-            bool stop = false;
-            if (pos < nbits) {
-                uint32_t sym, used;
-                if (decode_one(br, lut, root_bits, sym, used)) {
-                    pos += used;
-                    nd++;
-                    stop = op.sym(j, sym);
-                } else {
-                    pos = nbits;  // cannot happen on our own streams
-                }
+        bool have = false;
+        uint32_t sym = 0;
+        if (active && pos < nbits) {
+            uint32_t used;
+            if (decode_one(br, lut, root_bits, sym, used)) {
+                pos += used;
+                nd++;
+                have = true;
+            } else {
+                pos = nbits;  // cannot happen on our own streams
             }
-            if (stop || pos >= nbits) {
-                op.end(j, stop, nd, nbits);
-                active = false;
-            }
+        }
+        const bool stop = op.sym(have, sym, base + nd);  // all lanes (warp-level ops allowed)
+        if (active && (stop || pos >= nbits || nd >= lim)) {
+            op.end(j, seg0, stop, base + nd, nbits);
+            active = false;
         }
     }
 }
 
 struct FindOp {
-    const uint8_t* deleted;
-    const uint32_t* bits;
+    const uint32_t* deleted;
     const uint64_t* coff;
     const uint32_t* copied;
     const uint32_t* msize;
-    uint8_t* deleted_w;
+    const uint32_t* ncw;
+    uint32_t* deleted_w;
     uint32_t* hitlist;
+    uint32_t* hitnd;
+    uint32_t* hitx;
+    const uint8_t* segd;
+    const uint32_t* xfirst;
     RoundCtl* ctl;
-    uint32_t pick;
+    uint32_t pick, mark;
     uint64_t maxd = 0;
-    unsigned long long hv = 0, mv = 0, by = 0;
-    __device__ bool live(uint64_t i, uint32_t& j) {
-        j = (uint32_t)i;
-        return !deleted[i] && bits[i] != kDenseBits;
-    }
-    __device__ bool sym(uint32_t, uint32_t v) { return v == pick; }
-    __device__ void end(uint32_t j, bool stopped, uint32_t nd, uint32_t nbits) {
-        bool found = stopped;
-        const uint64_t c0 = coff[j], c1 = coff[j + 1];
-        if (!found)
-            for (uint64_t c = c0; c < c1; ++c)
-                if (copied[c] == pick) {
-                    found = true;
-                    break;
-                }
-        maxd = nd > maxd ? nd : maxd;
-        by += (nbits + 7) / 8 + 4 * (c1 - c0);
-        if (found) {
-            deleted_w[j] = 1;
-            hitlist[atomicAdd(&ctl->nhit, 1ull)] = j;
-            hv += msize[j];
-        } else {
-            mv += msize[j];
+    unsigned long long hv = 0, by = 0;
+    __device__ bool live(uint32_t j) const { return deleted[j] == 0; }
+    __device__ bool sym(bool have, uint32_t v, uint32_t) const { return have && v == pick; }
+    __device__ void hit(uint32_t j, uint32_t decoded) {
+        deleted_w[j] = mark;
+        hitlist[atomicAdd(&ctl->nhit, 1ull)] = j;
+        if (segd[j]) {  // the apply pass subtracts every segment of a hit
+            const uint32_t nx = (ncw[j] - 1) / kSegCodewords, x0 = xfirst[j];
+            const unsigned long long b = atomicAdd(&ctl->nhitx, (unsigned long long)nx);
+            for (uint32_t t = 0; t < nx; ++t) hitx[b + t] = x0 + t;
         }
+        hitnd[j] = decoded;
+        hv += msize[j];
+        maxd = decoded > maxd ? decoded : maxd;
+    }
+    __device__ void end(uint32_t j, bool seg0, bool stopped, uint32_t idx, uint32_t nbits) {
+        if (stopped) {  // pick is codeword idx-1 of the set: idx codewords decoded (huffman.cpp:148)
+            hit(j, idx);
+            return;
+        }
+        if (!seg0) return;
+        // once per set: the uncodable members, searched after the whole stream
+        const uint64_t c0 = coff[j], c1 = coff[j + 1];
+        by += (nbits + 7) / 8 + 4 * (c1 - c0);
+        for (uint64_t c = c0; c < c1; ++c)
+            if (copied[c] == pick) {
+                hit(j, ncw[j]);
+                return;
+            }
     }
 };
 
-// the warp's share of [0, count): contiguous ranges, one per warp of the grid
-__device__ __forceinline__ void warp_range(uint64_t count, uint64_t& lo, uint64_t& hi) {
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t per = (count + nw - 1) / nw;
-    lo = min(count, w * per);
-    hi = min(count, lo + per);
-}
-
-__global__ void k_huff_find(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
-                            const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
-                            const uint32_t* __restrict__ copied, const uint32_t* __restrict__ msize, uint64_t count,
+__global__ void k_huff_find(SegView sv, uint64_t total, uint32_t* __restrict__ list0, uint32_t* __restrict__ list1,
+                            const uint64_t* __restrict__ coff, const uint32_t* __restrict__ copied,
+                            const uint32_t* __restrict__ msize, const uint32_t* __restrict__ ncw,
+                            const uint8_t* __restrict__ segd, const uint32_t* __restrict__ xfirst,
                             const unsigned long long* __restrict__ lut, uint32_t root_bits, RoundCtl* ctl,
-                            uint8_t* __restrict__ deleted, uint32_t* __restrict__ hitlist,
-                            unsigned long long* __restrict__ maxdec, unsigned long long* __restrict__ alg_bytes) {
+                            uint32_t* __restrict__ deleted, uint32_t r, uint32_t* __restrict__ hitlist,
+                            uint32_t* __restrict__ hitx, uint32_t* __restrict__ hitnd,
+                            unsigned long long* __restrict__ maxdec, unsigned long long* __restrict__ alg_bytes,
+                            unsigned int* __restrict__ hist0, unsigned int* __restrict__ hist1, uint64_t n) {
     const uint32_t pick = ctl->pick;
     if (pick == 0xffffffffu) return;
-    FindOp op{deleted, bits, coff, copied, msize, deleted, hitlist, ctl, pick};
-    uint64_t lo, hi;
-    warp_range(count, lo, hi);
-    warp_decode_range(lo, hi, words, woff, bits, lut, root_bits, op);
-    warp_add_u64(&ctl->vol[0], op.hv);
-    warp_add_u64(&ctl->vol[1], op.mv);
+    {
+        // the spare table is the recount target of this round: clear it while decoding
+        const uint32_t cur = ctl->cur;
+        unsigned int* spare = cur ? hist0 : hist1;
+        for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+            spare[v] = 0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->cur_snap = cur;
+            ctl->live_snap = ctl->live_vol;
+        }
+    }
+    FindOp op{deleted, coff, copied, msize, ncw, deleted, hitlist, hitnd, hitx, segd, xfirst, ctl, pick, r + 1};
+    // round 0 walks every item and lists the ones it took (live at that point: the sets the
+    // first pick covers -- on hub-dominated inputs most of the large ones -- drop out);
+    // later rounds walk that list
+    if (r == 0)
+        warp_decode_items(&ctl->queue[0], RangeSrc{}, total, sv, lut, root_bits, op, list0, &ctl->nlist[0]);
+    else
+        warp_decode_items(&ctl->queue[0], ListSrc{list0}, ctl->nlist[0], sv, lut, root_bits, op);
+    warp_add_u64(&ctl->hvol, op.hv);
     warp_add_u64(alg_bytes, op.by);
     uint64_t local_max = op.maxd;
     for (int o = 16; o; o >>= 1) local_max = max(local_max, (uint64_t)__shfl_xor_sync(FULL, local_max, o));
@@ -386,11 +508,11 @@ __global__ void k_huff_find(const uint32_t* __restrict__ words, const uint64_t* 
 // hybrid bitmap sets, find pass: one thread per bitmap set (a bit test)
 __global__ void k_dense_find(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
                              const uint32_t* __restrict__ ids, const uint32_t* __restrict__ msize, uint64_t nd,
-                             RoundCtl* ctl, uint8_t* __restrict__ deleted, uint32_t* __restrict__ dround, uint32_t r,
-                             unsigned long long* __restrict__ alg_bytes) {
+                             RoundCtl* ctl, uint32_t* __restrict__ deleted, uint32_t r,
+                             uint32_t* __restrict__ hitnd, unsigned long long* __restrict__ alg_bytes) {
     const uint32_t pick = ctl->pick;
     if (pick == 0xffffffffu) return;
-    unsigned long long hv = 0, mv = 0, by = 0;
+    unsigned long long hv = 0, by = 0;
     for (uint64_t x0 = blockIdx.x * (uint64_t)blockDim.x; x0 < nd; x0 += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t x = x0 + threadIdx.x;
         if (x >= nd) continue;
@@ -398,100 +520,109 @@ __global__ void k_dense_find(const uint32_t* __restrict__ words, const uint64_t*
         if (deleted[j]) continue;
         by += 4;
         if ((__ldg(words + woff[j] + (pick >> 5)) >> (pick & 31)) & 1u) {
-            deleted[j] = 1;
-            dround[x] = r + 1;
+            deleted[j] = r + 1;
+            hitnd[j] = 0;  // nothing decoded (the oracle's bitmap sets leave the ledger alone)
             hv += msize[j];
-        } else {
-            mv += msize[j];
         }
     }
-    warp_add_u64(&ctl->vol[0], hv);
-    warp_add_u64(&ctl->vol[1], mv);
+    warp_add_u64(&ctl->hvol, hv);
     warp_add_u64(alg_bytes, by);
 }
 
-__global__ void k_round_decide(RoundCtl* ctl, uint64_t n) {
-    if (ctl->pick == 0xffffffffu) {
-        ctl->apply = kApplyNone;
-        return;
-    }
-    // recount = decode M members + clear n counters; subtract = decode H members
-    ctl->apply = ctl->vol[1] + n / 64 < ctl->vol[0] ? kApplyRecount : kApplySub;
-}
-
-__global__ void k_zero_if_recount(const RoundCtl* ctl, unsigned int* __restrict__ hist, uint64_t n) {
-    if (ctl->apply != kApplyRecount) return;
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
-        hist[v] = 0;
-}
-
-// apply pass: add `delta` for every member of the listed (subtract: this round's hits,
-// delta = -1 mod 2^32) or live (recount: select.cpp:196-199, delta = +1) sets
+// apply pass: add `delta` for every member of this round's hits (subtract, delta = -1 mod
+// 2^32, the pick skipped -- every hit holds it and its count becomes 0) or of the live sets
+// (recount into the cleared spare table, select.cpp:196-199)
 struct ApplyOp {
-    const uint8_t* deleted;     // recount: live = !deleted
-    const uint32_t* hitlist;    // subtract: the round's hits
-    const uint32_t* bits;
+    const uint32_t* deleted;
     const uint64_t* coff;
     const uint32_t* copied;
     unsigned int* hist;
     unsigned int delta;
+    uint32_t want;              // deleted mark of the sets taking part (0: live, r+1: hits)
+    uint32_t skip;
     unsigned long long by = 0;
-    __device__ bool live(uint64_t i, uint32_t& j) {
-        j = hitlist ? hitlist[i] : (uint32_t)i;
-        return (hitlist || !deleted[i]) && bits[j] != kDenseBits;
-    }
-    __device__ bool sym(uint32_t, uint32_t v) {
-        atomicAdd(&hist[v], delta);
+    __device__ bool live(uint32_t j) const { return deleted[j] == want; }
+    __device__ bool sym(bool have, uint32_t v, uint32_t) {
+        if (have && v != skip) atomicAdd(&hist[v], delta);
         return false;
     }
-    __device__ void end(uint32_t j, bool, uint32_t, uint32_t nbits) {
+    __device__ void end(uint32_t j, bool seg0, bool, uint32_t, uint32_t nbits) {
+        if (!seg0) return;
         const uint64_t c0 = coff[j], c1 = coff[j + 1];
-        for (uint64_t c = c0; c < c1; ++c) atomicAdd(&hist[copied[c]], delta);
+        for (uint64_t c = c0; c < c1; ++c) {
+            const uint32_t v = copied[c];
+            if (v != skip) atomicAdd(&hist[v], delta);
+        }
         by += (nbits + 7) / 8 + 4 * (c1 - c0);
     }
 };
 
-__global__ void k_huff_sub(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
-                           const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
-                           const uint32_t* __restrict__ copied, const unsigned long long* __restrict__ lut,
-                           uint32_t root_bits, const RoundCtl* ctl, const uint32_t* __restrict__ hitlist,
-                           unsigned int* __restrict__ hist, unsigned long long* __restrict__ alg_bytes) {
-    if (ctl->apply != kApplySub) return;
-    ApplyOp op{nullptr, hitlist, bits, coff, copied, hist, 0xffffffffu};
-    uint64_t lo, hi;
-    warp_range(ctl->nhit, lo, hi);
-    warp_decode_range(lo, hi, words, woff, bits, lut, root_bits, op);
-    warp_add_u64(alg_bytes, op.by);
-}
-
-__global__ void k_huff_recount(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
-                               const uint32_t* __restrict__ bits, const uint64_t* __restrict__ coff,
-                               const uint32_t* __restrict__ copied, uint64_t count,
-                               const unsigned long long* __restrict__ lut, uint32_t root_bits, const RoundCtl* ctl,
-                               const uint8_t* __restrict__ deleted, unsigned int* __restrict__ hist,
-                               unsigned long long* __restrict__ alg_bytes) {
-    if (ctl->apply != kApplyRecount) return;
-    ApplyOp op{deleted, nullptr, bits, coff, copied, hist, 1u};
-    uint64_t lo, hi;
-    warp_range(count, lo, hi);
-    warp_decode_range(lo, hi, words, woff, bits, lut, root_bits, op);
-    warp_add_u64(alg_bytes, op.by);
+// apply pass: the smaller of "subtract the hits" (H) and "recount the misses into the cleared
+// spare table" (M); block 0 publishes the choice and the table that is now live.  Also the
+// round's decode-buffer ledger entry for the misses (every codeword of a miss is decoded).
+__global__ void k_huff_apply(SegView sv, const uint32_t* __restrict__ list0, const uint32_t* __restrict__ list1,
+                             const uint32_t* __restrict__ hitlist, const uint32_t* __restrict__ hitx,
+                             const uint64_t* __restrict__ coff,
+                             const uint32_t* __restrict__ copied, const uint32_t* __restrict__ ncw,
+                             const unsigned long long* __restrict__ lut, uint32_t root_bits, RoundCtl* ctl,
+                             const uint32_t* __restrict__ deleted, uint32_t r, unsigned int* __restrict__ hist0,
+                             unsigned int* __restrict__ hist1, uint64_t n, unsigned long long* __restrict__ maxdec,
+                             unsigned long long* __restrict__ alg_bytes) {
+    if (ctl->pick == 0xffffffffu) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->apply = kApplyNone;
+        return;
+    }
+    const uint32_t cur = ctl->cur_snap;
+    const unsigned long long H = ctl->hvol, M = ctl->live_snap - H;
+    const bool recount = M + n / 64 < H;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->apply = recount ? kApplyRecount : kApplySub;
+        ctl->cur = recount ? cur ^ 1u : cur;
+        ctl->live_vol = M;
+    }
+    unsigned int* live = cur ? hist1 : hist0;
+    unsigned int* spare = cur ? hist0 : hist1;
+    {
+        // the misses: every codeword decoded (huffman.cpp:150-157)
+        uint64_t m = 0;
+        for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < sv.count;
+             j += (uint64_t)gridDim.x * blockDim.x)
+            if (deleted[j] == 0) m = max(m, (uint64_t)ncw[j]);
+        for (int o = 16; o; o >>= 1) m = max(m, (uint64_t)__shfl_xor_sync(FULL, m, o));
+        if ((threadIdx.x & 31) == 0 && m) atomicMax(maxdec, (unsigned long long)m);
+    }
+    const uint32_t pick = ctl->pick;
+    if (recount) {
+        // the live sets' items are among the items this round's find pass took
+        ApplyOp op{deleted, coff, copied, spare, 1u, 0u, 0xffffffffu};
+        warp_decode_items(&ctl->queue[1], ListSrc{list0}, ctl->nlist[0], sv, lut, root_bits, op);
+        warp_add_u64(alg_bytes, op.by);
+    } else {
+        ApplyOp op{deleted, coff, copied, live, 0xffffffffu, r + 1, pick};
+        const HitSrc hs{hitlist, hitx, ctl->nhit, sv.count};
+        warp_decode_items(&ctl->queue[1], hs, ctl->nhit + ctl->nhitx, sv, lut, root_bits, op);
+        warp_add_u64(alg_bytes, op.by);
+        if (blockIdx.x == 0 && threadIdx.x == 0) live[pick] = 0;
+    }
 }
 
 // hybrid bitmap sets, apply pass: CTA per bitmap set -- subtract this round's hits or
 // recount the live ones
 __global__ void k_dense_apply(const uint32_t* __restrict__ words, const uint64_t* __restrict__ woff,
                               const uint32_t* __restrict__ ids, uint64_t nd, uint64_t nwd, const RoundCtl* ctl,
-                              const uint8_t* __restrict__ deleted, const uint32_t* __restrict__ dround, uint32_t r,
-                              unsigned int* __restrict__ hist, unsigned long long* __restrict__ alg_bytes) {
+                              const uint32_t* __restrict__ deleted, uint32_t r, unsigned int* __restrict__ hist0,
+                              unsigned int* __restrict__ hist1, unsigned long long* __restrict__ alg_bytes) {
     const uint32_t apply = ctl->apply;
     if (apply == kApplyNone) return;
+    const uint32_t pick = ctl->pick;
+    // subtract: the live table of the round; recount: the spare one the apply pass filled
+    unsigned int* hist = (ctl->cur_snap ^ (apply == kApplyRecount ? 1u : 0u)) ? hist1 : hist0;
+    const uint32_t want = apply == kApplySub ? r + 1 : 0u;
+    const unsigned int delta = apply == kApplySub ? 0xffffffffu : 1u;
     uint64_t by = 0;
     for (uint64_t x = blockIdx.x; x < nd; x += gridDim.x) {
         const uint32_t j = ids[x];
-        const bool take = apply == kApplySub ? dround[x] == r + 1 : !deleted[j];
-        if (!take) continue;  // uniform over the CTA
-        const unsigned int delta = apply == kApplySub ? 0xffffffffu : 1u;
+        if (deleted[j] != want) continue;  // uniform over the CTA
         const uint32_t* bm = words + woff[j];
         by += 4 * nwd;
         for (uint64_t i = threadIdx.x; i < nwd; i += blockDim.x) {
@@ -499,7 +630,8 @@ __global__ void k_dense_apply(const uint32_t* __restrict__ words, const uint64_t
             while (m) {
                 const uint32_t b = __ffs(m) - 1;
                 m &= m - 1;
-                atomicAdd(&hist[(uint32_t)(i * 32 + b)], delta);
+                const uint32_t v = (uint32_t)(i * 32 + b);
+                if (apply != kApplySub || v != pick) atomicAdd(&hist[v], delta);
             }
         }
     }
@@ -546,11 +678,42 @@ __global__ void k_decode_find(const uint32_t* __restrict__ words, uint64_t woff,
     out[0] = 0;
 }
 
-__global__ void k_pick_from_key(const unsigned long long* __restrict__ keys, uint32_t r, uint8_t* __restrict__ is_seed,
-                                uint32_t* __restrict__ seeds, unsigned long long* __restrict__ marg, RoundCtl* ctl,
-                                uint64_t n) {
-    // padding persists: once a round had gain 0 the reference stops recounting (select.cpp:173-182)
-    const unsigned long long key = keys[r];
+// table_argmax (select.cpp:10-20) over the live table, then -- in the last block to finish --
+// the round's pick: padding once a round had gain 0 (select.cpp:173-182)
+__global__ void k_argmax_pick(const unsigned int* __restrict__ hist0, const unsigned int* __restrict__ hist1,
+                              uint64_t n, RoundCtl* ctl, unsigned long long* __restrict__ keys, uint32_t r,
+                              uint8_t* __restrict__ is_seed, uint32_t* __restrict__ seeds,
+                              unsigned long long* __restrict__ marg) {
+    const unsigned int* hist = ctl->cur ? hist1 : hist0;
+    unsigned long long best = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = ((unsigned long long)hist[v] << 32) | (0xffffffffu - (uint32_t)v);
+        best = key > best ? key : best;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(FULL, best, o);
+        best = x > best ? x : best;
+    }
+    __shared__ unsigned long long sb[32];
+    __shared__ bool last;
+    if ((threadIdx.x & 31) == 0) sb[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        best = threadIdx.x < (blockDim.x >> 5) ? sb[threadIdx.x] : 0;
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long x = __shfl_xor_sync(FULL, best, o);
+            best = x > best ? x : best;
+        }
+        if (threadIdx.x == 0) {
+            if (best) atomicMax(&keys[r], best);
+            __threadfence();
+            last = atomicAdd(&ctl->done, 1u) == gridDim.x - 1;
+        }
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    const unsigned long long key = atomicAdd(&keys[r], 0ull);
     uint32_t pick = key ? 0xffffffffu - (uint32_t)(key & 0xffffffffu) : 0;
     uint32_t gain = (uint32_t)(key >> 32);
     if (ctl->padding) gain = 0;
@@ -564,10 +727,21 @@ __global__ void k_pick_from_key(const unsigned long long* __restrict__ keys, uin
         ctl->pick = pick;
     }
     ctl->nhit = 0;
-    ctl->vol[0] = ctl->vol[1] = 0;
+    ctl->nhitx = 0;
+    ctl->hvol = 0;
+    ctl->queue[0] = ctl->queue[1] = 0;
+    ctl->done = 0;
     is_seed[pick] = 1;
     seeds[r] = pick;
     marg[r] = gain;
+}
+
+__global__ void k_seg_flags(const uint64_t* __restrict__ nx, const uint64_t* __restrict__ xoff, uint64_t cnt,
+                            uint64_t xbase, uint8_t* __restrict__ segd, uint32_t* __restrict__ xfirst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
+        segd[i] = nx[i] ? 1 : 0;
+        xfirst[i] = (uint32_t)(xbase + xoff[i]);
+    }
 }
 
 __global__ void k_add2(uint64_t* __restrict__ a, uint64_t* __restrict__ b, uint64_t cnt, uint64_t da, uint64_t db) {
@@ -618,10 +792,15 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     S.coff.reserve(base + cnt + 1, s);
     S.bits.reserve(base + cnt, s);
     S.msize.reserve(base + cnt, s);
-    DBuf<uint64_t> nwords, ncp;
+    S.ncw.reserve(base + cnt, s);
+    S.segd.reserve(base + cnt, s);
+    S.xfirst.reserve(base + cnt, s);
+    DBuf<uint64_t> nwords, ncp, nx, xoff;
     DBuf<uint8_t> swap;
     nwords.exact(cnt);
     ncp.exact(cnt);
+    nx.exact(cnt);
+    xoff.exact(cnt + 1);
     swap.exact(cnt);
     unsigned long long* d_payload = d.scal.p + 16;
     CK(cudaMemsetAsync(d_payload, 0, 8, s));
@@ -635,7 +814,7 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     k_enc_size<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_len.p, top,
                                                    S.bits.p + base, nwords.p, ncp.p, swap.p, d_payload,
                                                    S.hybrid ? S.n : 0, base, S.dense_ids.p, d_dense,
-                                                   S.msize.p + base);
+                                                   S.msize.p + base, S.ncw.p + base, nx.p);
     kt_size.stop();
     CK_LAUNCH("k_enc_size");
     d.kernel_launches++;
@@ -644,12 +823,17 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     cub::DeviceScan::InclusiveSum(nullptr, tb, nwords.p, S.woff.p + base + 1, cnt, s);
     size_t tb2 = 0;
     cub::DeviceScan::InclusiveSum(nullptr, tb2, ncp.p, S.coff.p + base + 1, cnt, s);
-    d.tmp.reserve(std::max(tb, tb2), s, false);
+    size_t tb3 = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb3, nx.p, xoff.p + 1, cnt, s);
+    d.tmp.reserve(std::max(std::max(tb, tb2), tb3), s, false);
     CK(cub::DeviceScan::InclusiveSum(d.tmp.p, tb, nwords.p, S.woff.p + base + 1, cnt, s));
     CK(cub::DeviceScan::InclusiveSum(d.tmp.p, tb2, ncp.p, S.coff.p + base + 1, cnt, s));
-    uint64_t add[2];
+    CK(cudaMemsetAsync(xoff.p, 0, 8, s));
+    CK(cub::DeviceScan::InclusiveSum(d.tmp.p, tb3, nx.p, xoff.p + 1, cnt, s));
+    uint64_t add[3];
     CK(cudaMemcpyAsync(&add[0], S.woff.p + base + cnt, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&add[1], S.coff.p + base + cnt, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&add[2], xoff.p + cnt, 8, cudaMemcpyDeviceToHost, s));
     unsigned long long payload = 0, dense_total = S.dense_count;
     CK(cudaMemcpyAsync(&payload, d_payload, 8, cudaMemcpyDeviceToHost, s));
     if (S.hybrid) CK(cudaMemcpyAsync(&dense_total, d_dense, 8, cudaMemcpyDeviceToHost, s));
@@ -670,14 +854,20 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
         CK_LAUNCH("k_add2");
         d.kernel_launches++;
     }
-    const uint64_t new_words = add[0], new_cp = add[1];
+    const uint64_t new_words = add[0], new_cp = add[1], new_x = add[2];
     S.words.reserve(w_total + new_words + 4, s);
     S.copied.reserve(c_total + new_cp + 1, s);
+    if (S.n_extra + new_x >= 0xffffffffULL - (base + cnt)) fail(IMMX_EINVAL, "store too large for the select index");
+    S.xset.reserve(S.n_extra + new_x + 1, s);
+    S.xbit.reserve(S.n_extra + new_x + 1, s);
+    k_seg_flags<<<grid_for(cnt, d), 256, 0, s>>>(nx.p, xoff.p, cnt, S.n_extra, S.segd.p + base, S.xfirst.p + base);
+    d.kernel_launches++;
     CK(cudaMemsetAsync(S.words.p + w_total, 0, (new_words + 4) * 4, s));
     kt_pack.start(&d, IMMX_KSTAT_ENCODE);
     k_enc_pack<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_bits.p, S.code_len.p,
                                                    top, swap.p, S.woff.p + base, S.coff.p + base, S.words.p,
-                                                   S.copied.p, S.bits.p + base);
+                                                   S.copied.p, S.bits.p + base, xoff.p, base, S.xset.p + S.n_extra,
+                                                   S.xbit.p + S.n_extra);
     kt_pack.stop();
     CK_LAUNCH("k_enc_pack");
     d.kernel_launches++;
@@ -693,6 +883,7 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     }
     S.total_words = w_total + new_words;
     S.total_copied = c_total + new_cp;
+    S.n_extra += new_x;
     S.count = base + cnt;
     S.payload_bytes += payload;
     if (payload_out) *payload_out = payload;
@@ -724,6 +915,26 @@ void store_append_host(Store& S, const uint8_t* bytes, uint64_t n_bytes, uint64_
     // member count unknown without decoding: an upper bound (it only steers select's apply pass)
     const uint32_t msz = (uint32_t)std::min<uint64_t>(bit_length + n_cp, 0xffffffffULL);
     CK(cudaMemcpyAsync(S.msize.p + base, &msz, 4, cudaMemcpyHostToDevice, s));
+    // codeword count (select's decode-buffer ledger) by one counting decode; no checkpoints
+    S.ncw.reserve(base + 1, s);
+    S.segd.reserve(base + 1, s);
+    S.xfirst.reserve(base + 1, s);
+    {
+        DBuf<uint32_t> dec;
+        dec.exact(bit_length + 1);
+        long long* out = reinterpret_cast<long long*>(d.scal.p + 26);
+        k_decode_find<<<1, 32, 0, s>>>(S.words.p, S.total_words, b32, S.copied.p, 0, 0, S.lut.p, S.lut_root_bits,
+                                       0xffffffffu, dec.p, out);
+        CK_LAUNCH("k_decode_find");
+        d.kernel_launches++;
+        long long h[2];
+        CK(cudaMemcpyAsync(h, out, 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const uint32_t cw = (uint32_t)h[1];
+        const uint8_t z = 0;
+        CK(cudaMemcpyAsync(S.ncw.p + base, &cw, 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(S.segd.p + base, &z, 1, cudaMemcpyHostToDevice, s));
+    }
     CK(cudaStreamSynchronize(s));
     S.total_words = wo;
     S.total_copied = co;
@@ -768,16 +979,25 @@ int store_decode_find(const Store& S, uint64_t j, uint32_t top, std::vector<uint
 }
 
 // select.cpp:150-230 on the device.  d_hist: the encoding-time table (u32, consumed).
+static bool debug_select() {
+    static const bool on = [] {
+        const char* e = std::getenv("IMMX_DEBUG_SELECT");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+
 void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& out, std::vector<uint64_t>* maxdec) {
     Device& d = *S.dev;
     cudaStream_t s = d.stream;
     const uint64_t theta = S.count, n = S.n;
     if (theta == 0) fail(IMMX_EINVAL, "selection requires at least one set");
     if (k >= n) fail(IMMX_EINVAL, "selection requires k < n");
-    DBuf<uint8_t> deleted, is_seed;
+    DBuf<uint32_t> deleted;  // 0: live; r+1: covered in round r
+    DBuf<uint8_t> is_seed;
     deleted.exact(theta);
     is_seed.exact(n);
-    CK(cudaMemsetAsync(deleted.p, 0, theta, s));
+    CK(cudaMemsetAsync(deleted.p, 0, theta * 4, s));
     CK(cudaMemsetAsync(is_seed.p, 0, n, s));
     DBuf<unsigned long long> keys, marg, mdec;
     keys.exact(k);
@@ -785,44 +1005,66 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
     mdec.exact(k);
     CK(cudaMemsetAsync(keys.p, 0, k * 8, s));
     CK(cudaMemsetAsync(mdec.p, 0, k * 8, s));
-    DBuf<uint32_t> seeds, hitlist, dround;
+    const uint64_t items = theta + S.n_extra;
+    DBuf<uint32_t> seeds, hitlist, hitnd, hitx, list0, list1;  // list1: unused (kept for the signature)
     seeds.exact(k);
     hitlist.exact(theta);
-    dround.exact(std::max<uint64_t>(S.dense_count, 1));
-    CK(cudaMemsetAsync(dround.p, 0, std::max<uint64_t>(S.dense_count, 1) * 4, s));
+    hitnd.exact(theta);
+    hitx.exact(std::max<uint64_t>(S.n_extra, 1));
+    list0.exact(items);
+    list1.exact(1);
     DBuf<unsigned long long> ctlbuf;
     ctlbuf.exact((sizeof(RoundCtl) + 7) / 8);
     RoundCtl* ctl = reinterpret_cast<RoundCtl*>(ctlbuf.p);
-    CK(cudaMemsetAsync(ctl, 0, sizeof(RoundCtl), s));
-    const unsigned grid = grid_for(theta, d);
-    const unsigned grid_n = grid_for(n, d);
+    {
+        RoundCtl h{};
+        h.live_vol = 0;
+        CK(cudaMemcpyAsync(ctl, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    }
+    // live member volume = sum of msize
+    {
+        size_t tb = 0;
+        cub::DeviceReduce::Sum(nullptr, tb, S.msize.p, &ctl->live_vol, theta, s);
+        d.tmp.reserve(tb, s, false);
+        CK(cub::DeviceReduce::Sum(d.tmp.p, tb, S.msize.p, &ctl->live_vol, theta, s));
+    }
+    // persistent decode grid: 5 CTAs of 8 warps per SM, fewer for small stores
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)d.num_sms * 5, (items + 255) / 256));
     const uint64_t nd = S.dense_count, nwd = (n + 31) / 32;
+    SegView sv{S.words.p, S.woff.p, S.bits.p, S.segd.p, S.xset.p, S.xbit.p, S.xfirst.p, theta};
     DBuf<unsigned long long> rbytes;
     rbytes.exact(k);
     CK(cudaMemsetAsync(rbytes.p, 0, k * 8, s));
+    DBuf<unsigned int> hist_b;  // the second table (recount target, double-buffered)
+    hist_b.exact(n);
+    const unsigned grid_am = grid_for(n, d);
     std::vector<KTimer> kt(k);
     for (uint32_t r = 0; r < k; ++r) {
-        argmax_dev(d, d_hist, n, keys.p + r);
-        k_pick_from_key<<<1, 1, 0, s>>>(keys.p, r, is_seed.p, seeds.p, marg.p, ctl, n);
+        k_argmax_pick<<<grid_am, 256, 0, s>>>(d_hist, hist_b.p, n, ctl, keys.p, r, is_seed.p, seeds.p, marg.p);
         kt[r].start(&d, IMMX_KSTAT_HSELECT);
-        k_huff_find<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, S.msize.p, theta,
-                                         S.lut.p, S.lut_root_bits, ctl, deleted.p, hitlist.p, mdec.p + r,
-                                         rbytes.p + r);
+        k_huff_find<<<grid, 256, 0, s>>>(sv, items, list0.p, list1.p, S.coff.p, S.copied.p, S.msize.p, S.ncw.p,
+                                         S.segd.p, S.xfirst.p, S.lut.p, S.lut_root_bits, ctl, deleted.p, r,
+                                         hitlist.p, hitx.p, hitnd.p, mdec.p + r, rbytes.p + r, d_hist, hist_b.p, n);
         if (nd)
             k_dense_find<<<grid_for(nd, d), 256, 0, s>>>(S.words.p, S.woff.p, S.dense_ids.p, S.msize.p, nd, ctl,
-                                                         deleted.p, dround.p, r, rbytes.p + r);
-        k_round_decide<<<1, 1, 0, s>>>(ctl, n);
-        k_zero_if_recount<<<grid_n, 256, 0, s>>>(ctl, d_hist, n);
-        k_huff_sub<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, S.lut.p,
-                                        S.lut_root_bits, ctl, hitlist.p, d_hist, rbytes.p + r);
-        k_huff_recount<<<grid, 256, 0, s>>>(S.words.p, S.woff.p, S.bits.p, S.coff.p, S.copied.p, theta, S.lut.p,
-                                            S.lut_root_bits, ctl, deleted.p, d_hist, rbytes.p + r);
+                                                         deleted.p, r, hitnd.p, rbytes.p + r);
+        k_huff_apply<<<grid, 256, 0, s>>>(sv, list0.p, list1.p, hitlist.p, hitx.p, S.coff.p, S.copied.p, S.ncw.p,
+                                          S.lut.p, S.lut_root_bits, ctl, deleted.p, r, d_hist, hist_b.p, n,
+                                          mdec.p + r, rbytes.p + r);
         if (nd)
             k_dense_apply<<<(unsigned)std::min<uint64_t>(nd, (uint64_t)d.num_sms * 8), 256, 0, s>>>(
-                S.words.p, S.woff.p, S.dense_ids.p, nd, nwd, ctl, deleted.p, dround.p, r, d_hist, rbytes.p + r);
+                S.words.p, S.woff.p, S.dense_ids.p, nd, nwd, ctl, deleted.p, r, d_hist, hist_b.p, rbytes.p + r);
         kt[r].stop();
+        if (debug_select()) {
+            RoundCtl h;
+            CK(cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            std::fprintf(stderr, "[immx select] round %u pick %u apply %u hits %llu H %llu live %llu\n", r, h.pick,
+                         h.apply, (unsigned long long)h.nhit, (unsigned long long)h.hvol,
+                         (unsigned long long)h.live_vol);
+        }
         CK_LAUNCH("select_huffman round");
-        d.kernel_launches += 6 + (nd ? 2 : 0);
+        d.kernel_launches += 3 + (nd ? 2 : 0);
     }
     std::vector<unsigned long long> hbytes(k);
     CK(cudaMemcpyAsync(hbytes.data(), rbytes.p, k * 8, cudaMemcpyDeviceToHost, s));

@@ -166,6 +166,18 @@ struct Store {
     DBuf<uint64_t> woff;   // count+1 word offsets
     DBuf<uint32_t> bits;   // count
     DBuf<uint32_t> msize;  // count: members per set (steers select's apply pass)
+    DBuf<uint32_t> ncw;    // count: codewords per set (0 for hybrid bitmap sets)
+    // decode checkpoints (a side index; the streams are unchanged): every kSegCodewords-th
+    // codeword of a longer set starts an extra segment -- set and bit offset; a set's extra
+    // segments are contiguous from xfirst[j] -- so select decodes one large set on many lanes
+    DBuf<uint8_t> segd;    // count: 1 if the set has extra segments
+    DBuf<uint32_t> xfirst; // count: index of the set's first extra segment
+    DBuf<uint32_t> xset, xbit;
+    uint64_t n_extra = 0;
+    uint64_t device_bytes() const {  // the store as held in HBM, side index included
+        return total_words * 4 + total_copied * 4 + (count + 1) * 16 + count * (4 + 4 + 4 + 1 + 4) + n_extra * 8 +
+               dense_count * 4;
+    }
     DBuf<uint64_t> coff;   // count+1
     DBuf<uint32_t> words;
     DBuf<uint32_t> copied;
@@ -178,6 +190,7 @@ struct Store {
     DBuf<uint32_t> dense_ids;  // store indices of the dense sets
 };
 constexpr uint32_t kDenseBits = 0xffffffffu;
+constexpr uint32_t kSegCodewords = 64;
 
 
 // ---------------------------------------------------------------- device operations ----
