@@ -112,6 +112,7 @@ struct Device {
     // grow-only workspaces reused across calls (a run allocates them once; later runs and
     // later estimation iterations reuse them, so the allocator never churns on GB buffers)
     DBuf<uint32_t> ws_list[2], ws_nospace, ws_qscratch, ws_gbits;
+    DBuf<uint32_t> ws_pbits, ws_pq, ws_pbusy;  // sampler promotion slots
     DBuf<unsigned long long> ws_ctl;
     DBuf<unsigned int> ws_hist;
     DBuf<uint64_t> ws_idx_off, ws_cnt64;

@@ -24,6 +24,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.hpp"
 
@@ -321,6 +322,7 @@ struct SampCtl {
     unsigned long long edges;
     unsigned long long members;
     unsigned long long edges_abandoned;  // scanned by samples that moved to the next tier
+    unsigned long long n_promoted;       // samples that continued in a promotion slot
 };
 
 struct SampJob {
@@ -342,6 +344,12 @@ struct SampJob {
     uint32_t* gbits;                 // per-warp global bitmap (GlobBits tier)
     uint32_t qcap;
     int model;
+    // promotion slots (hash tiers): a sample outgrowing its shared-memory hash takes a slot
+    // -- a global visited bitmap (pwords words) and a queue of pqcap members -- and continues
+    uint32_t* pbits;
+    uint32_t* pq;
+    uint32_t* pbusy;
+    uint32_t npslots, pqcap, pwords;
 };
 
 enum VisKind { kVisSmemBits = 0, kVisHash11 = 1, kVisHash13 = 2, kVisHash15 = 3, kVisGlobBits = 4 };
@@ -533,6 +541,7 @@ struct BlkSmem {
     uint32_t nextrow[2][NW];  // rows of the next group's warp starts (double-buffered)
     uint32_t nextpos[2];      // the gpos those rows were computed for
     uint32_t hdup;            // hash tiers: duplicate keys left by conflict rollbacks
+    int pslot;                // hash tiers: the promotion slot taken (-1: none)
     uint32_t lpos[NW * 32 * U];  // rare path: success positions
     uint32_t lv[NW * 32 * U];    //            and targets
     uint32_t cut;
@@ -591,7 +600,11 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
     constexpr uint32_t G = NW * 32 * U;
     const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t lt = lanemask_lt();
-    uint32_t* q = job.qscratch + (size_t)blockIdx.x * job.qcap;
+    constexpr bool kHash = KIND == kBHash13 || KIND == kBHash15;
+    uint32_t* const qbase = job.qscratch + (size_t)blockIdx.x * job.qcap;
+    uint32_t* q = qbase;
+    uint32_t qcap = job.qcap;
+    uint32_t* pw = nullptr;  // promoted: the slot's global visited bitmap (CTA-uniform)
     typename BVisOf<KIND>::T vis;
     if constexpr (KIND == kBBits) {
         vis.w = dsm;
@@ -639,285 +652,352 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
         uint64_t edges = 0;
         bool overflow = false;
         __syncthreads();
-        while (qhead < qlen && !overflow) {
-            // ---- batch of rows q[qhead .. qhead+nb) ----
-            const uint32_t nb = min(NB, qlen - qhead);
-            uint32_t deg = 0;
-            uint64_t rs = 0, th = g.gthr;
-            if (tid < nb) {
-                const uint32_t u = q[qhead + tid];
-                rs = g.row[u];
-                deg = (uint32_t)(g.row[u + 1] - rs);
-                if (PM == kProbRow) th = g.thr[u];
-            }
-            uint32_t x = deg;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(FULL, x, o);
-                if (lane >= (uint32_t)o) x += y;
-            }
-            // rows without edges are compacted away: every remaining row holds >= 1 edge, so a
-            // window of 32 positions meets at most 33 rows (the mask mapping below needs that)
-            const uint32_t nem = __ballot_sync(FULL, deg > 0);
-            if (lane == 31) {
-                sh.wsum[w] = x;
-                sh.wsum2[w] = __popc(nem);
-            }
-            __syncthreads();
-            uint32_t off, total, coff, nrows;
-            warp_prefix<NW>(sh.wsum, w, off, total);
-            warp_prefix<NW>(sh.wsum2, w, coff, nrows);
-            if (deg > 0) {
-                const uint32_t c = coff + __popc(nem & lt);
-                sh.cum[c] = x + off;
-                sh.rs[c] = rs - (uint64_t)(x + off - deg);  // col index of flattened position p = rs + p
-                if (PM == kProbRow) sh.thr[c] = th;
-            }
-            if (tid >= nrows) sh.cum[tid] = total;
-            __syncthreads();
-            edges += total;
-            qhead += nb;
-            uint32_t gpos = 0;
-            uint32_t r_w = 0;  // row holding this warp's first position (monotone over the batch)
-            uint32_t par = 0;  // group parity (double buffer of the precomputed start rows)
-            if (tid < 2) sh.nextpos[tid] = 0xffffffffu;
-            __syncthreads();
-            while (gpos < total) {
-                // ---- one group: positions gpos + (w*U + i)*32 + lane ----
-                uint32_t v[U];
-                uint64_t T[U];
-                bool cand[U];
-                uint32_t dm[U];
-                uint32_t wd = 0;
-                const uint32_t a0 = gpos + w * U * 32;
-                const uint32_t a0c = min(a0, total - 1);
-                if (sh.nextpos[par] == gpos && a0 < total) r_w = sh.nextrow[par][w];  // precomputed
-                else r_w = advance_row<NW>(sh.cum, r_w, a0c);
-                if (w == 0) {
-                    // the next group's warp starts (valid unless a conflict cut moves gpos):
-                    // NW parallel searches in lanes 0..NW-1, published by this group's barriers
-                    const uint32_t x = gpos + G + lane * U * 32;
-                    if (lane < (uint32_t)NW && x < total) sh.nextrow[par ^ 1][lane] = advance_row<NW>(sh.cum, r_w, x);
-                    if (lane == 0) sh.nextpos[par ^ 1] = gpos + G;
-                }
-                // this warp's slice leaves the row holding gpos -> the group spans several rows
-                bool my_multi = false;
-                if (a0 < total && sh.cum[r_w] >= min(a0 + U * 32, total)) {
-                    my_multi = r_w && sh.cum[r_w - 1] > gpos;
-                    // fast path: the warp's whole slice lies in row r_w
-                    const uint64_t base = sh.rs[r_w];
-                    const uint64_t Trow = PM == kProbRow ? sh.thr[r_w] : g.gthr;
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        const uint32_t e = a0 + i * 32 + lane;
-                        const bool valid = e < total;
-                        v[i] = valid ? __ldg(g.col + base + e) : 0u;
-                        if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + base + e) : 0ull;
-                        else T[i] = Trow;
-                    }
-                } else {
-                    // the slice crosses rows.  Per sub-window starting at position a in row r:
-                    // lane j looks at the start of row r+1+j (= cum[r+j]); the OR of the bits
-                    // (start - a - 1) over the warp marks the row starts inside (a, a+32], so
-                    // lane l's row is r + popc(starts at offsets 1..l) and the next sub-window
-                    // starts in row r + popc(all) -- no loop, no search (rows are non-empty).
-                    my_multi = a0 < total;
-                    uint32_t r = r_w;
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        const uint32_t a = a0 + i * 32;
-                        const uint32_t e = a + lane;
-                        const bool valid = e < total;
-                        const uint32_t ec = min(e, total - 1);
-                        const uint32_t rel = sh.cum[min(r + lane, NB - 1)] - a;  // >= 1
-                        const uint32_t M = __reduce_or_sync(FULL, rel - 1 < 32 ? 1u << (rel - 1) : 0u);
-                        const uint32_t rr = min(r + __popc(M & ((1u << lane) - 1u)), NB - 1);
-                        r = min(r + __popc(M), NB - 1);
-                        const uint64_t eg = sh.rs[rr] + (uint64_t)ec;
-                        v[i] = valid ? __ldg(g.col + eg) : 0u;
-                        if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + eg) : 0ull;
-                        else if (PM == kProbRow) T[i] = sh.thr[rr];
-                        else T[i] = g.gthr;
+        bool want_promote = false, no_slot = false;
+        // the sample's BFS; P: the visited set is a promotion slot's global bitmap (compiled as
+        // its own loop, so the hash path carries no per-probe test)
+        auto run = [&](auto ptag) {
+            constexpr bool P = decltype(ptag)::value;
+            auto vhas = [&](uint32_t v) -> bool {
+                if constexpr (P) return (__ldcg(pw + (v >> 5)) >> (v & 31)) & 1u;
+                else return vis.has(v);
+            };
+            auto vadd = [&](uint32_t v) -> bool {
+                if constexpr (P) return atomicOr(pw + (v >> 5), 1u << (v & 31)) & (1u << (v & 31));
+                else return vis.add_test(v);
+            };
+            while (qhead < qlen && !overflow) {
+                if constexpr (kHash && !P) {
+                    // halfway to the hash's capacity: continue in a promotion slot (uniform test)
+                    if (job.npslots && !no_slot && qlen + sh.hdup > qcap / 2) {
+                        want_promote = true;
+                        return;
                     }
                 }
-#pragma unroll
-                for (int i = 0; i < U; ++i) {
-                    const bool valid = a0 + i * 32 + lane < total;
-                    cand[i] = valid && T[i] != kThrNever && !vis.has(v[i]);
-                    dm[i] = __ballot_sync(FULL, cand[i] && T[i] != kThrAlways);
-                    wd += __popc(dm[i]);
+                // ---- batch of rows q[qhead .. qhead+nb) ----
+                const uint32_t nb = min(NB, qlen - qhead);
+                uint32_t deg = 0;
+                uint64_t rs = 0, th = g.gthr;
+                if (tid < nb) {
+                    const uint32_t u = q[qhead + tid];
+                    rs = g.row[u];
+                    deg = (uint32_t)(g.row[u + 1] - rs);
+                    if (PM == kProbRow) th = g.thr[u];
                 }
-                if (lane == 0) sh.wsum[w] = wd;
-                // barrier + "does the group span several rows" in one instruction
-                const bool multi = __syncthreads_or(my_multi) || g.row_dups;
-                uint32_t dbefore, dtotal;
-                warp_prefix<NW>(sh.wsum, w, dbefore, dtotal);
-                bool succ[U];
-                uint32_t sm[U];
-                uint32_t ws = 0;
-                uint64_t tb = t + dbefore;
-#pragma unroll
-                for (int i = 0; i < U; ++i) {
-                    const bool coin = coin_success(s0, tb + __popc(dm[i] & lt), T[i]);  // branch-free
-                    succ[i] = cand[i] && (T[i] == kThrAlways || coin);
-                    tb += __popc(dm[i]);
-                    sm[i] = __ballot_sync(FULL, succ[i]);
-                    ws += __popc(sm[i]);
+                uint32_t x = deg;
+    #pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, x, o);
+                    if (lane >= (uint32_t)o) x += y;
                 }
-                if (lane == 0) sh.wsum2[w] = ws;
-                // Insert the successes before the barrier (which then also publishes them) when
-                // the visited set cannot overflow: bitmap tiers hold all n; a hash tier has room
-                // for a whole group.  Otherwise check the capacity first (stotal may count a
-                // repeated target twice -- then the sample just moves to the next tier).
-                const bool early = KIND == kBBits || KIND == kBGlob || qlen + sh.hdup + G <= job.qcap;
-                bool flag = false;
-                if (early) {
-#pragma unroll
-                    for (int i = 0; i < U; ++i)
-                        if (succ[i]) flag |= vis.add_test(v[i]);
+                // rows without edges are compacted away: every remaining row holds >= 1 edge, so a
+                // window of 32 positions meets at most 33 rows (the mask mapping below needs that)
+                const uint32_t nem = __ballot_sync(FULL, deg > 0);
+                if (lane == 31) {
+                    sh.wsum[w] = x;
+                    sh.wsum2[w] = __popc(nem);
                 }
                 __syncthreads();
-                uint32_t sbefore, stotal;
-                warp_prefix<NW>(sh.wsum2, w, sbefore, stotal);
-                if (!early) {
-                    if (qlen + sh.hdup + stotal > job.qcap) {
-                        overflow = true;
-                        break;
-                    }
-#pragma unroll
-                    for (int i = 0; i < U; ++i)
-                        if (succ[i]) flag |= vis.add_test(v[i]);
-                    __syncthreads();
+                uint32_t off, total, coff, nrows;
+                warp_prefix<NW>(sh.wsum, w, off, total);
+                warp_prefix<NW>(sh.wsum2, w, coff, nrows);
+                if (deg > 0) {
+                    const uint32_t c = coff + __popc(nem & lt);
+                    sh.cum[c] = x + off;
+                    sh.rs[c] = rs - (uint64_t)(x + off - deg);  // col index of flattened position p = rs + p
+                    if (PM == kProbRow) sh.thr[c] = th;
                 }
-                // a single-row group has distinct targets: no success can repeat a target
-                bool conflict = false;
-                if (multi) {
-#pragma unroll
-                    for (int i = 0; i < U; ++i)
-                        if (cand[i] && !succ[i] && vis.has(v[i])) flag = true;
-                    conflict = __syncthreads_or(flag);
-                }
-                if (!conflict) {
-                    // common case: commit the whole group
-                    uint32_t p = qlen + sbefore;
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        if (succ[i]) q[p + __popc(sm[i] & lt)] = v[i];
-                        p += __popc(sm[i]);
+                if (tid >= nrows) sh.cum[tid] = total;
+                __syncthreads();
+                edges += total;
+                qhead += nb;
+                uint32_t gpos = 0;
+                uint32_t r_w = 0;  // row holding this warp's first position (monotone over the batch)
+                uint32_t par = 0;  // group parity (double buffer of the precomputed start rows)
+                if (tid < 2) sh.nextpos[tid] = 0xffffffffu;
+                __syncthreads();
+                while (gpos < total) {
+                    // ---- one group: positions gpos + (w*U + i)*32 + lane ----
+                    uint32_t v[U];
+                    uint64_t T[U];
+                    bool cand[U];
+                    uint32_t dm[U];
+                    uint32_t wd = 0;
+                    const uint32_t a0 = gpos + w * U * 32;
+                    const uint32_t a0c = min(a0, total - 1);
+                    if (sh.nextpos[par] == gpos && a0 < total) r_w = sh.nextrow[par][w];  // precomputed
+                    else r_w = advance_row<NW>(sh.cum, r_w, a0c);
+                    if (w == 0) {
+                        // the next group's warp starts (valid unless a conflict cut moves gpos):
+                        // NW parallel searches in lanes 0..NW-1, published by this group's barriers
+                        const uint32_t x = gpos + G + lane * U * 32;
+                        if (lane < (uint32_t)NW && x < total) sh.nextrow[par ^ 1][lane] = advance_row<NW>(sh.cum, r_w, x);
+                        if (lane == 0) sh.nextpos[par ^ 1] = gpos + G;
                     }
-                    qlen += stotal;
-                    t += dtotal;
-                    gpos += G;
-                    par ^= 1;
-                } else {
-                    // rare: resolve the first position whose target repeats an earlier success
-                    {
-                        uint32_t p = sbefore;
-#pragma unroll
+                    // this warp's slice leaves the row holding gpos -> the group spans several rows
+                    bool my_multi = false;
+                    if (a0 < total && sh.cum[r_w] >= min(a0 + U * 32, total)) {
+                        my_multi = r_w && sh.cum[r_w - 1] > gpos;
+                        // fast path: the warp's whole slice lies in row r_w
+                        const uint64_t base = sh.rs[r_w];
+                        const uint64_t Trow = PM == kProbRow ? sh.thr[r_w] : g.gthr;
+    #pragma unroll
                         for (int i = 0; i < U; ++i) {
-                            if (succ[i]) {
-                                const uint32_t k = p + __popc(sm[i] & lt);
-                                sh.lpos[k] = gpos + (w * U + i) * 32 + lane;
-                                sh.lv[k] = v[i];
-                            }
+                            const uint32_t e = a0 + i * 32 + lane;
+                            const bool valid = e < total;
+                            v[i] = valid ? __ldg(g.col + base + e) : 0u;
+                            if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + base + e) : 0ull;
+                            else T[i] = Trow;
+                        }
+                    } else {
+                        // the slice crosses rows.  Per sub-window starting at position a in row r:
+                        // lane j looks at the start of row r+1+j (= cum[r+j]); the OR of the bits
+                        // (start - a - 1) over the warp marks the row starts inside (a, a+32], so
+                        // lane l's row is r + popc(starts at offsets 1..l) and the next sub-window
+                        // starts in row r + popc(all) -- no loop, no search (rows are non-empty).
+                        my_multi = a0 < total;
+                        uint32_t r = r_w;
+    #pragma unroll
+                        for (int i = 0; i < U; ++i) {
+                            const uint32_t a = a0 + i * 32;
+                            const uint32_t e = a + lane;
+                            const bool valid = e < total;
+                            const uint32_t ec = min(e, total - 1);
+                            const uint32_t rel = sh.cum[min(r + lane, NB - 1)] - a;  // >= 1
+                            const uint32_t M = __reduce_or_sync(FULL, rel - 1 < 32 ? 1u << (rel - 1) : 0u);
+                            const uint32_t rr = min(r + __popc(M & ((1u << lane) - 1u)), NB - 1);
+                            r = min(r + __popc(M), NB - 1);
+                            const uint64_t eg = sh.rs[rr] + (uint64_t)ec;
+                            v[i] = valid ? __ldg(g.col + eg) : 0u;
+                            if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + eg) : 0ull;
+                            else if (PM == kProbRow) T[i] = sh.thr[rr];
+                            else T[i] = g.gthr;
+                        }
+                    }
+    #pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        const bool valid = a0 + i * 32 + lane < total;
+                        cand[i] = valid && T[i] != kThrNever && !vhas(v[i]);
+                        dm[i] = __ballot_sync(FULL, cand[i] && T[i] != kThrAlways);
+                        wd += __popc(dm[i]);
+                    }
+                    if (lane == 0) sh.wsum[w] = wd;
+                    // barrier + "does the group span several rows" in one instruction
+                    const bool multi = __syncthreads_or(my_multi) || g.row_dups;
+                    uint32_t dbefore, dtotal;
+                    warp_prefix<NW>(sh.wsum, w, dbefore, dtotal);
+                    bool succ[U];
+                    uint32_t sm[U];
+                    uint32_t ws = 0;
+                    uint64_t tb = t + dbefore;
+    #pragma unroll
+                    for (int i = 0; i < U; ++i) {
+                        const bool coin = coin_success(s0, tb + __popc(dm[i] & lt), T[i]);  // branch-free
+                        succ[i] = cand[i] && (T[i] == kThrAlways || coin);
+                        tb += __popc(dm[i]);
+                        sm[i] = __ballot_sync(FULL, succ[i]);
+                        ws += __popc(sm[i]);
+                    }
+                    if (lane == 0) sh.wsum2[w] = ws;
+                    // Insert the successes before the barrier (which then also publishes them) when
+                    // the visited set cannot overflow: bitmap tiers hold all n; a hash tier has room
+                    // for a whole group.  Otherwise check the capacity first (stotal may count a
+                    // repeated target twice -- then the sample just moves to the next tier).
+                    const bool early = P ? qlen + G <= qcap
+                                         : (KIND == kBBits || KIND == kBGlob || qlen + sh.hdup + G <= qcap);
+                    bool flag = false;
+                    if (early) {
+    #pragma unroll
+                        for (int i = 0; i < U; ++i)
+                            if (succ[i]) flag |= vadd(v[i]);
+                    }
+                    __syncthreads();
+                    uint32_t sbefore, stotal;
+                    warp_prefix<NW>(sh.wsum2, w, sbefore, stotal);
+                    if (!early) {
+                        if (qlen + (P ? 0u : sh.hdup) + stotal > qcap) {
+                            overflow = true;
+                            break;
+                        }
+    #pragma unroll
+                        for (int i = 0; i < U; ++i)
+                            if (succ[i]) flag |= vadd(v[i]);
+                        __syncthreads();
+                    }
+                    // a single-row group has distinct targets: no success can repeat a target
+                    bool conflict = false;
+                    if (multi) {
+    #pragma unroll
+                        for (int i = 0; i < U; ++i)
+                            if (cand[i] && !succ[i] && vhas(v[i])) flag = true;
+                        conflict = __syncthreads_or(flag);
+                    }
+                    if (!conflict) {
+                        // common case: commit the whole group
+                        uint32_t p = qlen + sbefore;
+    #pragma unroll
+                        for (int i = 0; i < U; ++i) {
+                            if (succ[i]) q[p + __popc(sm[i] & lt)] = v[i];
                             p += __popc(sm[i]);
                         }
+                        qlen += stotal;
+                        t += dtotal;
+                        gpos += G;
+                        par ^= 1;
+                    } else {
+                        // rare: resolve the first position whose target repeats an earlier success
+                        {
+                            uint32_t p = sbefore;
+    #pragma unroll
+                            for (int i = 0; i < U; ++i) {
+                                if (succ[i]) {
+                                    const uint32_t k = p + __popc(sm[i] & lt);
+                                    sh.lpos[k] = gpos + (w * U + i) * 32 + lane;
+                                    sh.lv[k] = v[i];
+                                }
+                                p += __popc(sm[i]);
+                            }
+                        }
+                        if (tid == 0) sh.cut = 0xffffffffu;
+                        __syncthreads();
+    #pragma unroll
+                        for (int i = 0; i < U; ++i) {
+                            if (!cand[i] || !vhas(v[i])) continue;
+                            const uint32_t pos = gpos + (w * U + i) * 32 + lane;
+                            uint32_t minp = 0xffffffffu;
+                            for (uint32_t k = 0; k < stotal; ++k)
+                                if (sh.lv[k] == v[i]) minp = min(minp, sh.lpos[k]);
+                            if (minp < pos) atomicMin(&sh.cut, pos);
+                        }
+                        __syncthreads();
+                        const uint32_t cut = sh.cut;
+                        // counts of draws / successes before the cut
+                        uint32_t wd2 = 0, ws2 = 0;
+    #pragma unroll
+                        for (int i = 0; i < U; ++i) {
+                            const uint32_t a = gpos + (w * U + i) * 32;
+                            const uint32_t keep = cut == 0xffffffffu ? FULL
+                                                : (cut <= a ? 0u : (cut - a >= 32 ? FULL : ((1u << (cut - a)) - 1u)));
+                            wd2 += __popc(dm[i] & keep);
+                            ws2 += __popc(sm[i] & keep);
+                            sm[i] &= keep;
+                        }
+                        __syncthreads();
+                        if (lane == 0) {
+                            sh.wsum[w] = wd2;
+                            sh.wsum2[w] = ws2;
+                        }
+                        __syncthreads();
+                        uint32_t d2b = 0, d2t = 0, s2b = 0, s2t = 0;
+    #pragma unroll
+                        for (int k = 0; k < NW; ++k) {
+                            const uint32_t c = sh.wsum[k], c2 = sh.wsum2[k];
+                            d2b += (uint32_t)k < w ? c : 0u;
+                            d2t += c;
+                            s2b += (uint32_t)k < w ? c2 : 0u;
+                            s2t += c2;
+                        }
+                        uint32_t p = qlen + s2b;
+    #pragma unroll
+                        for (int i = 0; i < U; ++i) {
+                            if ((sm[i] >> lane) & 1u) q[p + __popc(sm[i] & lt)] = v[i];
+                            p += __popc(sm[i]);
+                        }
+                        qlen += s2t;
+                        t += d2t;
+                        if (cut != 0xffffffffu) {
+                            bool bitmap_vis = KIND == kBBits || KIND == kBGlob;
+                            uint32_t* bw = nullptr;
+                            if constexpr (KIND == kBBits || KIND == kBGlob) bw = vis.w;
+                            if constexpr (P) {
+                                bitmap_vis = true;
+                                bw = pw;
+                            }
+                            if (bitmap_vis) {
+                                // roll back the successes at or after the cut, then restore the
+                                // committed ones (a repeated target may have shared a bit)
+    #pragma unroll
+                                for (int i = 0; i < U; ++i)
+                                    if (succ[i] && gpos + (w * U + i) * 32 + lane >= cut)
+                                        atomicAnd(&bw[v[i] >> 5], ~(1u << (v[i] & 31)));
+                                __syncthreads();
+    #pragma unroll
+                                for (int i = 0; i < U; ++i)
+                                    if ((sm[i] >> lane) & 1u) atomicOr(&bw[v[i] >> 5], 1u << (v[i] & 31));
+                            } else if constexpr (kHash) {
+                              if (qlen + sh.hdup + G <= qcap) {
+                                // hash: empty the slots of the post-cut successes (located first, then
+                                // cleared: a concurrent probe must not see a half-cleared chain), then
+                                // re-insert the committed successes of this group.  Keys from earlier
+                                // groups never probe through a slot that was empty when they were
+                                // inserted, so their chains stay intact; a committed key may end up
+                                // stored twice -- counted in hdup so the load stays <= 1/2.
+                                uint32_t slot[U];
+    #pragma unroll
+                                for (int i = 0; i < U; ++i)
+                                    slot[i] = (succ[i] && gpos + (w * U + i) * 32 + lane >= cut) ? vis.find(v[i])
+                                                                                                : 0xffffffffu;
+                                __syncthreads();
+    #pragma unroll
+                                for (int i = 0; i < U; ++i)
+                                    if (slot[i] != 0xffffffffu) vis.s[slot[i]] = kEmptyKey;
+                                __syncthreads();
+    #pragma unroll
+                                for (int i = 0; i < U; ++i)
+                                    if ((sm[i] >> lane) & 1u) vis.add_test(v[i]);
+                                if (tid == 0) sh.hdup += s2t;
+                            } else {
+                                // rebuild the visited set from the committed members
+                                __syncthreads();
+                                vis.clear_all();
+                                __syncthreads();
+                                for (uint32_t k = tid; k < qlen; k += blockDim.x) vis.add_test(q[k]);
+                                if (tid == 0) sh.hdup = 0;
+                              }
+                            }
+                        }
+                        gpos = cut == 0xffffffffu ? gpos + G : cut;
+                        par ^= 1;
+                        __syncthreads();  // rare path: rebuilt visited set, smem success list reuse
                     }
-                    if (tid == 0) sh.cut = 0xffffffffu;
-                    __syncthreads();
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        if (!cand[i] || !vis.has(v[i])) continue;
-                        const uint32_t pos = gpos + (w * U + i) * 32 + lane;
-                        uint32_t minp = 0xffffffffu;
-                        for (uint32_t k = 0; k < stotal; ++k)
-                            if (sh.lv[k] == v[i]) minp = min(minp, sh.lpos[k]);
-                        if (minp < pos) atomicMin(&sh.cut, pos);
-                    }
-                    __syncthreads();
-                    const uint32_t cut = sh.cut;
-                    // counts of draws / successes before the cut
-                    uint32_t wd2 = 0, ws2 = 0;
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        const uint32_t a = gpos + (w * U + i) * 32;
-                        const uint32_t keep = cut == 0xffffffffu ? FULL
-                                            : (cut <= a ? 0u : (cut - a >= 32 ? FULL : ((1u << (cut - a)) - 1u)));
-                        wd2 += __popc(dm[i] & keep);
-                        ws2 += __popc(sm[i] & keep);
-                        sm[i] &= keep;
-                    }
-                    __syncthreads();
-                    if (lane == 0) {
-                        sh.wsum[w] = wd2;
-                        sh.wsum2[w] = ws2;
-                    }
-                    __syncthreads();
-                    uint32_t d2b = 0, d2t = 0, s2b = 0, s2t = 0;
-#pragma unroll
-                    for (int k = 0; k < NW; ++k) {
-                        const uint32_t c = sh.wsum[k], c2 = sh.wsum2[k];
-                        d2b += (uint32_t)k < w ? c : 0u;
-                        d2t += c;
-                        s2b += (uint32_t)k < w ? c2 : 0u;
-                        s2t += c2;
-                    }
-                    uint32_t p = qlen + s2b;
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        if ((sm[i] >> lane) & 1u) q[p + __popc(sm[i] & lt)] = v[i];
-                        p += __popc(sm[i]);
-                    }
-                    qlen += s2t;
-                    t += d2t;
-                    if (cut != 0xffffffffu) {
-                        if constexpr (KIND == kBBits || KIND == kBGlob) {
-                            // roll back the successes at or after the cut, then restore the
-                            // committed ones (a repeated target may have shared a bit)
-#pragma unroll
-                            for (int i = 0; i < U; ++i)
-                                if (succ[i] && gpos + (w * U + i) * 32 + lane >= cut)
-                                    atomicAnd(&vis.w[v[i] >> 5], ~(1u << (v[i] & 31)));
-                            __syncthreads();
-#pragma unroll
-                            for (int i = 0; i < U; ++i)
-                                if ((sm[i] >> lane) & 1u) vis.add_test(v[i]);
-                        } else if (qlen + sh.hdup + G <= job.qcap) {
-                            // hash: empty the slots of the post-cut successes (located first, then
-                            // cleared: a concurrent probe must not see a half-cleared chain), then
-                            // re-insert the committed successes of this group.  Keys from earlier
-                            // groups never probe through a slot that was empty when they were
-                            // inserted, so their chains stay intact; a committed key may end up
-                            // stored twice -- counted in hdup so the load stays <= 1/2.
-                            uint32_t slot[U];
-#pragma unroll
-                            for (int i = 0; i < U; ++i)
-                                slot[i] = (succ[i] && gpos + (w * U + i) * 32 + lane >= cut) ? vis.find(v[i])
-                                                                                            : 0xffffffffu;
-                            __syncthreads();
-#pragma unroll
-                            for (int i = 0; i < U; ++i)
-                                if (slot[i] != 0xffffffffu) vis.s[slot[i]] = kEmptyKey;
-                            __syncthreads();
-#pragma unroll
-                            for (int i = 0; i < U; ++i)
-                                if ((sm[i] >> lane) & 1u) vis.add_test(v[i]);
-                            if (tid == 0) sh.hdup += s2t;
-                        } else {
-                            // rebuild the visited set from the committed members
-                            __syncthreads();
-                            vis.clear_all();
-                            __syncthreads();
-                            for (uint32_t k = tid; k < qlen; k += blockDim.x) vis.add_test(q[k]);
-                            if (tid == 0) sh.hdup = 0;
+                }
+                __syncthreads();  // the batch's queue writes before the next batch reads them
+            }
+        };
+        run(std::false_type{});
+        if constexpr (kHash) {
+            if (want_promote) {
+                // take a slot: copy the members into its bitmap and queue, go on there
+                if (tid == 0) {
+                    int got = -1;
+                    for (uint32_t k = 0; k < job.npslots; ++k) {
+                        const uint32_t sl = (blockIdx.x + k) % job.npslots;
+                        if (atomicCAS(job.pbusy + sl, 0u, 1u) == 0u) {
+                            got = (int)sl;
+                            break;
                         }
                     }
-                    gpos = cut == 0xffffffffu ? gpos + G : cut;
-                    par ^= 1;
-                    __syncthreads();  // rare path: rebuilt visited set, smem success list reuse
+                    sh.pslot = got;
+                    if (got >= 0) atomicAdd(&job.ctl->n_promoted, 1ull);
+                }
+                __syncthreads();
+                if (sh.pslot >= 0) {
+                    uint32_t* nq = job.pq + (size_t)sh.pslot * job.pqcap;
+                    uint32_t* nw = job.pbits + (size_t)sh.pslot * job.pwords;
+                    for (uint32_t k = tid; k < qlen; k += blockDim.x) {
+                        const uint32_t v = q[k];
+                        nq[k] = v;
+                        atomicOr(nw + (v >> 5), 1u << (v & 31));
+                    }
+                    __syncthreads();
+                    q = nq;
+                    qcap = job.pqcap;
+                    pw = nw;
+                    run(std::true_type{});
+                } else {
+                    no_slot = true;
+                    run(std::false_type{});
                 }
             }
-            __syncthreads();  // the batch's queue writes before the next batch reads them
         }
         __syncthreads();
         if (!overflow) {
@@ -940,6 +1020,19 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
             atomicAdd(&job.ctl->edges_abandoned, (unsigned long long)edges);
         }
         __syncthreads();
+        if constexpr (kHash) {
+            if (pw) {  // hand the slot back clean: clear the members' words, then release
+                for (uint32_t k = tid; k < qlen; k += blockDim.x) pw[q[k] >> 5] = 0u;
+                __syncthreads();
+                if (tid == 0) {
+                    __threadfence();
+                    atomicExch(job.pbusy + sh.pslot, 0u);
+                }
+                pw = nullptr;
+                q = qbase;
+                qcap = job.qcap;
+            }
+        }
         vis.clear_members(q, qlen);
         __syncthreads();
     }
@@ -1027,6 +1120,14 @@ void launch_tier(Device& d, const GView& gv, SampJob job, const Tier& tier, uint
     kern<<<blocks, wpb * 32, smem, d.stream>>>(gv, job, tier.smem_words_per_warp);
     CK_LAUNCH("rrr_kernel");
     d.kernel_launches++;
+}
+
+bool promote_enabled() {  // IMMX_NO_PROMOTE=1 restarts overflowing samples on the next tier instead
+    static const bool on = [] {
+        const char* e = std::getenv("IMMX_NO_PROMOTE");
+        return !(e && *e && *e != '0');
+    }();
+    return on;
 }
 
 bool debug_tiers() {
@@ -1128,6 +1229,26 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
 
     GView gv = make_view(G);
     SampJob job{};
+    if (model == IMMX_MODEL_IC && nwords * 4 > 64 * 1024) {
+        // promotion slots for the hash tier: one per resident CTA where ~4 GB allow, each a
+        // visited bitmap over n and a queue of up to 2^17 members (larger samples move on to
+        // the global-bitmap tier)
+        const uint64_t pq = std::min<uint64_t>(G.n, 1u << 17);
+        const uint64_t slot_bytes = nwords * 4 + pq * 4;
+        const uint64_t nslots =
+            std::min<uint64_t>((uint64_t)d.num_sms * 4, std::max<uint64_t>(8, (4ULL << 30) / slot_bytes));
+        d.ws_pbits.reserve(nslots * nwords, s, false);
+        d.ws_pq.reserve(nslots * pq, s, false);
+        d.ws_pbusy.reserve(nslots, s, false);
+        CK(cudaMemsetAsync(d.ws_pbits.p, 0, nslots * nwords * 4, s));
+        CK(cudaMemsetAsync(d.ws_pbusy.p, 0, nslots * 4, s));
+        job.pbits = d.ws_pbits.p;
+        job.pq = d.ws_pq.p;
+        job.pbusy = d.ws_pbusy.p;
+        job.npslots = promote_enabled() ? (uint32_t)nslots : 0u;
+        job.pqcap = (uint32_t)pq;
+        job.pwords = (uint32_t)nwords;
+    }
     job.seed = seed;
     job.first = first;
     job.roots = d_roots;
@@ -1199,10 +1320,10 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         members += hctl->members;
         const uint32_t n_ovf = hctl->n_ovf, n_nospace = hctl->n_nospace;
         if (debug_tiers())
-            std::fprintf(stderr, "[immx sampler] tier %d%s items %u ovf %u nospace %u members %llu edges %llu abandoned %llu %.3f ms\n",
+            std::fprintf(stderr, "[immx sampler] tier %d%s items %u ovf %u nospace %u members %llu edges %llu abandoned %llu promoted %llu %.3f ms\n",
                          tier.kind, tier.block ? "b" : "w", nitems, n_ovf, n_nospace,
                          (unsigned long long)hctl->members, (unsigned long long)hctl->edges,
-                         (unsigned long long)hctl->edges_abandoned,
+                         (unsigned long long)hctl->edges_abandoned, (unsigned long long)hctl->n_promoted,
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_launch).count());
         {
             // algorithmic bytes of the samples this launch committed
