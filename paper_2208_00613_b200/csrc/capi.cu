@@ -482,7 +482,7 @@ void immx_pool_destroy(immx_pool* p) { delete p; }
 int immx_pool_clear(immx_pool* p) {
     return guard([&] {
         need(p, "pool");
-        p->p.count = p->p.members = p->p.edges = p->p.arena_used = 0;
+        pool_reset(p->p);
     });
 }
 int immx_pool_sample(immx_pool* p, const immx_graph* g, uint64_t count, uint64_t first, uint64_t seed, int model) {
@@ -615,7 +615,7 @@ int immx_estimate_theta(const immx_graph* g, uint32_t k, double eps, uint64_t se
         need(g, "graph");
         need(out, "out");
         if (keep) {
-            keep->p.count = keep->p.members = keep->p.edges = keep->p.arena_used = 0;
+            pool_reset(keep->p);
             estimate_theta_dev(g->g, k, eps, seed, model, keep->p, *out);
         } else {
             Pool tmp;
@@ -851,7 +851,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         }
         R->pool = d.run_pool;
         Pool& pool = R->pool->p;
-        pool.count = pool.members = pool.edges = pool.arena_used = 0;
+        pool_reset(pool);
 
         // ---- theta estimation (pipeline.cpp:61-63) ----
         auto t0 = Clock::now();
@@ -876,7 +876,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                 samples_drawn += theta - plan.estimation_samples;
             }
         } else {
-            pool.count = pool.members = pool.edges = pool.arena_used = 0;
+            pool_reset(pool);
         }
         int mode = IMMX_MODE_RAW, char_mode = IMMX_MODE_RAW;
         double t_codebook = 0.0, t_lut = 0.0;  // host: Huffman tree, decode table

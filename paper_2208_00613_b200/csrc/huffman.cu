@@ -638,6 +638,107 @@ __global__ void k_dense_apply(const uint32_t* __restrict__ words, const uint64_t
     if (threadIdx.x == 0 && by) atomicAdd(alg_bytes, (unsigned long long)by);
 }
 
+// ---- select_raw rounds (select.cpp:89-148) -------------------------------------------
+// The same round scheme on the raw pool: the sets holding the pick come from the inverted
+// index (one chunk per estimation iteration); the table is the old one minus the hits'
+// members or a recount of the live sets into the cleared spare table, whichever is smaller.
+struct RawChunkView {
+    const uint64_t* off;
+    const uint32_t* idx;
+};
+
+__global__ void k_index_fill_range(const uint32_t* __restrict__ arena, const uint64_t* __restrict__ off,
+                                   const uint32_t* __restrict__ len, uint64_t lo, uint64_t hi,
+                                   unsigned long long* __restrict__ cursor, uint32_t* __restrict__ idx) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t j = lo + w; j < hi; j += nw) {
+        const uint64_t b = off[j];
+        const uint32_t l = len[j];
+        for (uint32_t i = lane; i < l; i += 32) idx[atomicAdd(&cursor[arena[b + i]], 1ULL)] = (uint32_t)j;
+    }
+}
+
+__global__ void k_add_u32(unsigned int* __restrict__ a, const unsigned int* __restrict__ b, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] += b[i];
+}
+
+// find: the live sets holding the pick, from every index chunk; clears the spare table
+__global__ void k_raw_mark(const RawChunkView* __restrict__ chunks, uint32_t nch, RoundCtl* ctl,
+                           uint32_t* __restrict__ covered, const uint32_t* __restrict__ len, uint32_t r,
+                           uint32_t* __restrict__ hitlist, unsigned int* __restrict__ hist0,
+                           unsigned int* __restrict__ hist1, uint64_t n) {
+    const uint32_t pick = ctl->pick;
+    if (pick == 0xffffffffu) return;
+    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gs = (uint64_t)gridDim.x * blockDim.x;
+    {
+        const uint32_t cur = ctl->cur;
+        unsigned int* spare = cur ? hist0 : hist1;
+        for (uint64_t v = gt; v < n; v += gs) spare[v] = 0;
+        if (gt == 0) {
+            ctl->cur_snap = cur;
+            ctl->live_snap = ctl->live_vol;
+        }
+    }
+    unsigned long long hv = 0;
+    for (uint32_t c = 0; c < nch; ++c) {
+        const uint64_t b0 = chunks[c].off[pick], b1 = chunks[c].off[pick + 1];
+        for (uint64_t q = b0 + gt; q < b1; q += gs) {
+            const uint32_t sidx = chunks[c].idx[q];
+            if (covered[sidx] == 0) {  // a set holds the pick once: no two threads see it
+                covered[sidx] = r + 1;
+                hitlist[atomicAdd(&ctl->nhit, 1ull)] = sidx;
+                hv += len[sidx];
+            }
+        }
+    }
+    warp_add_u64(&ctl->hvol, hv);
+}
+
+// apply: subtract the hits' members (warp per hit) or recount the live sets (warp per set)
+__global__ void k_raw_apply(const uint32_t* __restrict__ arena, const uint64_t* __restrict__ off,
+                            const uint32_t* __restrict__ len, uint64_t count, RoundCtl* ctl,
+                            const uint32_t* __restrict__ covered, const uint32_t* __restrict__ hitlist,
+                            unsigned int* __restrict__ hist0, unsigned int* __restrict__ hist1, uint64_t n) {
+    const uint32_t pick = ctl->pick;
+    if (pick == 0xffffffffu) return;
+    const uint32_t cur = ctl->cur_snap;
+    const unsigned long long H = ctl->hvol, M = ctl->live_snap - H;
+    const bool recount = M + n / 64 < H;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->apply = recount ? kApplyRecount : kApplySub;
+        ctl->cur = recount ? cur ^ 1u : cur;
+        ctl->live_vol = M;
+    }
+    unsigned int* live = cur ? hist1 : hist0;
+    unsigned int* spare = cur ? hist0 : hist1;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    if (recount) {
+        for (uint64_t j = w; j < count; j += nw) {
+            if (covered[j]) continue;
+            const uint64_t b = off[j];
+            const uint32_t l = len[j];
+            for (uint32_t i = lane; i < l; i += 32) atomicAdd(&spare[arena[b + i]], 1u);
+        }
+    } else {
+        const uint64_t nh = ctl->nhit;
+        for (uint64_t x = w; x < nh; x += nw) {
+            const uint32_t j = hitlist[x];
+            const uint64_t b = off[j];
+            const uint32_t l = len[j];
+            for (uint32_t i = lane; i < l; i += 32) {
+                const uint32_t v = arena[b + i];
+                if (v != pick) atomicSub(&live[v], 1u);
+            }
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) live[pick] = 0;  // every hit held it
+    }
+}
+
 // decode_find on one set with every reference corruption check (huffman.cpp:129-158)
 // out[0]=status (1 found, 0 not, -2 invalid codeword, -3 mid-codeword), out[1]=n decoded
 __global__ void k_decode_find(const uint32_t* __restrict__ words, uint64_t woff, uint32_t nbits,
@@ -1078,6 +1179,108 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
     CK(cudaStreamSynchronize(s));
     finish_select(hseeds, hmarg, theta, out);
     if (maxdec) maxdec->assign(hmd.begin(), hmd.end());
+}
+
+// select.cpp:89-148 on the device (the estimation loop's greedy and raw mode).
+void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
+    Device& d = *P.dev;
+    cudaStream_t s = d.stream;
+    const uint64_t theta = P.count;
+    if (theta == 0) fail(IMMX_EINVAL, "selection requires at least one set");
+    if (k >= n) fail(IMMX_EINVAL, "selection requires k < n");
+    if (theta >= 0xffffffffULL) fail(IMMX_EINVAL, "more than 2^32-1 sets");
+    // the index: reuse the chunks of earlier calls on this pool, add one for the new sets
+    Pool& Pm = const_cast<Pool&>(P);
+    if (!Pm.rix) Pm.rix = std::make_shared<RawIndex>();
+    RawIndex& X = *Pm.rix;
+    if (X.epoch != P.epoch || X.n != n || X.indexed > theta) {
+        X.chunks.clear();
+        X.indexed = 0;
+        X.epoch = P.epoch;
+        X.n = n;
+        X.hist.exact(n);
+        CK(cudaMemsetAsync(X.hist.p, 0, n * 4, s));
+    }
+    if (X.indexed < theta) {
+        const uint64_t lo = X.indexed, hi = theta;
+        auto ch = std::make_unique<RawIndex::Chunk>();
+        DBuf<unsigned int> cnt;
+        cnt.exact(n);
+        CK(cudaMemsetAsync(cnt.p, 0, n * 4, s));
+        pool_hist_dev(P, lo, hi, cnt.p);
+        k_add_u32<<<grid_for(n, d), 256, 0, s>>>(X.hist.p, cnt.p, n);
+        DBuf<uint64_t> c64;
+        c64.exact(n + 1);
+        CK(cudaMemsetAsync(c64.p, 0, 8, s));
+        u32_to_u64_dev(d, cnt.p, n, c64.p + 1);
+        ch->off.exact(n + 1);
+        size_t tb = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tb, c64.p, ch->off.p, n + 1, s);
+        d.tmp.reserve(tb, s, false);
+        CK(cub::DeviceScan::InclusiveSum(d.tmp.p, tb, c64.p, ch->off.p, n + 1, s));
+        uint64_t tot = 0;
+        CK(cudaMemcpyAsync(&tot, ch->off.p + n, 8, cudaMemcpyDeviceToHost, s));
+        DBuf<unsigned long long> cursor;
+        cursor.exact(n + 1);
+        CK(cudaMemcpyAsync(cursor.p, ch->off.p, (n + 1) * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        ch->idx.exact(std::max<uint64_t>(tot, 1));
+        k_index_fill_range<<<grid_for((hi - lo) * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, cursor.p,
+                                                                      ch->idx.p);
+        CK_LAUNCH("k_index_fill_range");
+        d.kernel_launches += 3;
+        X.chunks.push_back(std::move(ch));
+        X.indexed = theta;
+        std::vector<RawChunkView> views;
+        for (auto& c : X.chunks) views.push_back({c->off.p, c->idx.p});
+        X.meta.exact((views.size() * sizeof(RawChunkView) + 7) / 8);
+        CK(cudaMemcpyAsync(X.meta.p, views.data(), views.size() * sizeof(RawChunkView), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    const uint32_t nch = (uint32_t)X.chunks.size();
+    DBuf<unsigned int>& hist = d.ws_hist;  // the working table (+ its double)
+    hist.exact(2 * n);
+    CK(cudaMemcpyAsync(hist.p, X.hist.p, n * 4, cudaMemcpyDeviceToDevice, s));
+    DBuf<uint32_t> covered, hitlist, seeds;  // covered: 0 live, r+1 covered in round r
+    DBuf<uint8_t> is_seed;
+    covered.exact(theta);
+    hitlist.exact(theta);
+    seeds.exact(k);
+    is_seed.exact(n);
+    CK(cudaMemsetAsync(covered.p, 0, theta * 4, s));
+    CK(cudaMemsetAsync(is_seed.p, 0, n, s));
+    DBuf<unsigned long long> keys, marg, ctlbuf;
+    keys.exact(k);
+    marg.exact(k);
+    CK(cudaMemsetAsync(keys.p, 0, k * 8, s));
+    ctlbuf.exact((sizeof(RoundCtl) + 7) / 8);
+    RoundCtl* ctl = reinterpret_cast<RoundCtl*>(ctlbuf.p);
+    {
+        RoundCtl h{};
+        h.live_vol = P.members;
+        CK(cudaMemcpyAsync(ctl, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    }
+    const unsigned grid_am = grid_for(n, d), grid_w = (unsigned)d.num_sms * 8;
+    const RawChunkView* views = reinterpret_cast<const RawChunkView*>(X.meta.p);
+    std::vector<KTimer> kt(k);
+    for (uint32_t r = 0; r < k; ++r) {
+        k_argmax_pick<<<grid_am, 256, 0, s>>>(hist.p, hist.p + n, n, ctl, keys.p, r, is_seed.p, seeds.p, marg.p);
+        kt[r].start(&d, IMMX_KSTAT_RSELECT);
+        k_raw_mark<<<grid_w, 256, 0, s>>>(views, nch, ctl, covered.p, P.len.p, r, hitlist.p, hist.p, hist.p + n, n);
+        k_raw_apply<<<grid_w, 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, theta, ctl, covered.p, hitlist.p, hist.p,
+                                           hist.p + n, n);
+        kt[r].stop();
+        CK_LAUNCH("select_raw round");
+        d.kernel_launches += 3;
+    }
+    CK(cudaStreamSynchronize(s));
+    for (uint32_t r = 0; r < k; ++r) kt[r].finish(0);
+    std::vector<uint32_t> hseeds(k);
+    std::vector<unsigned long long> hmarg(k);
+    CK(cudaMemcpyAsync(hseeds.data(), seeds.p, k * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hmarg.data(), marg.p, k * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    finish_select(hseeds, hmarg, theta, out);
 }
 
 // D2H of sets [lo,hi) in the reference's byte layout

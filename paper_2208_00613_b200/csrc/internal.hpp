@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "immx_b200.h"
@@ -140,6 +141,20 @@ struct DevGraph {
 
 // Raw RRR pool: sets live in an arena (bump-allocated chunks); set j of the pool is
 // arena[off[j] .. off[j]+len[j]).  Sets are appended in batches of global indices.
+// select_raw's inverted index over a pool, kept across calls: the estimation loop only
+// appends sets, so each call indexes just the new ones (one chunk per call) and keeps a
+// running vertex histogram
+struct RawIndex {
+    uint64_t epoch = ~0ULL, n = 0, indexed = 0;
+    DBuf<unsigned int> hist;  // counts over sets [0, indexed)
+    struct Chunk {
+        DBuf<uint64_t> off;   // n+1 offsets into idx
+        DBuf<uint32_t> idx;   // set ids, grouped by vertex
+    };
+    std::vector<std::unique_ptr<Chunk>> chunks;
+    DBuf<unsigned long long> meta;  // device copy of the chunks' {off, idx} pointers
+};
+
 struct Pool {
     Device* dev = nullptr;
     DBuf<uint32_t> arena;
@@ -151,7 +166,13 @@ struct Pool {
     uint64_t edges = 0;          // sum of edges scanned while sampling
     uint64_t arena_used = 0;     // arena cursor (host copy after each batch)
     DBuf<unsigned long long> cur;  // the cursor itself
+    uint64_t epoch = 0;          // bumped when the pool is emptied (invalidates rix)
+    std::shared_ptr<RawIndex> rix;
 };
+inline void pool_reset(Pool& P) {
+    P.count = P.members = P.edges = P.arena_used = 0;
+    ++P.epoch;
+}
 
 // Huffman-encoded store.  Set j: words[woff[j] ..] holds its MSB-first byte stream
 // (bytes in stream order in memory), bits[j] its bit length; copied[coff[j] .. coff[j+1]).

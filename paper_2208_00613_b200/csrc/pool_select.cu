@@ -249,68 +249,6 @@ void finish_select(const std::vector<uint32_t>& seeds, const std::vector<unsigne
 }
 
 // select_raw over all pool sets
-void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
-    Device& d = *P.dev;
-    cudaStream_t s = d.stream;
-    const uint64_t theta = P.count;
-    if (theta == 0) fail(IMMX_EINVAL, "selection requires at least one set");
-    if (k >= n) fail(IMMX_EINVAL, "selection requires k < n");
-    // device workspaces (grow-only, reused by every estimation iteration and run)
-    DBuf<unsigned int>& hist = d.ws_hist;
-    hist.exact(n);
-    CK(cudaMemsetAsync(hist.p, 0, n * 4, s));
-    pool_hist_dev(P, 0, theta, hist.p);
-    // inverted index: idx_off = exclusive scan of counts (u64)
-    DBuf<uint64_t>& idx_off = d.ws_idx_off;
-    idx_off.exact(n + 1);
-    DBuf<unsigned long long>& cursor = d.ws_cursor;
-    cursor.exact(n + 1);
-    {
-        DBuf<uint64_t>& cnt64 = d.ws_cnt64;
-        cnt64.exact(n + 1);
-        CK(cudaMemsetAsync(cnt64.p, 0, (n + 1) * 8, s));
-        u32_to_u64_dev(d, hist.p, n, cnt64.p + 1);
-        size_t tb = 0;
-        cub::DeviceScan::InclusiveSum(nullptr, tb, cnt64.p, idx_off.p, n + 1, s);
-        d.tmp.reserve(tb, s, false);
-        CK(cub::DeviceScan::InclusiveSum(d.tmp.p, tb, cnt64.p, idx_off.p, n + 1, s));
-        CK(cudaMemcpyAsync(cursor.p, idx_off.p, (n + 1) * 8, cudaMemcpyDeviceToDevice, s));
-        CK(cudaStreamSynchronize(s));
-    }
-    DBuf<uint32_t>& idx = d.ws_idx;
-    if (idx.cap < P.members) idx.exact(P.members + P.members / 2 + 1024);  // grows geometrically
-    k_index_fill<<<grid_for(theta * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, theta, cursor.p, idx.p);
-    CK_LAUNCH("k_index_fill");
-    d.kernel_launches++;
-    DBuf<uint8_t>& covered = d.ws_covered;
-    DBuf<uint8_t>& is_seed = d.ws_is_seed;
-    covered.exact(theta);
-    is_seed.exact(n);
-    CK(cudaMemsetAsync(covered.p, 0, theta, s));
-    CK(cudaMemsetAsync(is_seed.p, 0, n, s));
-    DBuf<unsigned long long> keys, marg;
-    keys.exact(k);
-    marg.exact(k);
-    CK(cudaMemsetAsync(keys.p, 0, k * 8, s));
-    DBuf<uint32_t> seeds, cover_pick;
-    seeds.exact(k);
-    cover_pick.exact(1);
-    const unsigned cover_grid = (unsigned)d.num_sms * 8;
-    for (uint32_t r = 0; r < k; ++r) {
-        argmax_dev(d, hist.p, n, keys.p + r);
-        k_round_pick<<<1, 1, 0, s>>>(keys.p, r, is_seed.p, seeds.p, marg.p, cover_pick.p, n);
-        k_cover_raw<<<cover_grid, 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, idx_off.p, idx.p, cover_pick.p,
-                                              covered.p, hist.p);
-        CK_LAUNCH("select_raw round");
-        d.kernel_launches += 2;
-    }
-    std::vector<uint32_t> hseeds(k);
-    std::vector<unsigned long long> hmarg(k);
-    CK(cudaMemcpyAsync(hseeds.data(), seeds.p, k * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hmarg.data(), marg.p, k * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    finish_select(hseeds, hmarg, theta, out);
-}
 
 // D2H gather of sets [lo, hi): offsets relative (hi-lo+1), members
 void pool_read_host(const Pool& P, uint64_t lo, uint64_t hi, uint64_t* offsets, uint32_t* members) {
