@@ -1050,7 +1050,10 @@ struct Tier {
     uint32_t max_blocks = 0;       // 0 = occupancy-limited
 };
 
-constexpr int kBlkNW = 8;
+#ifndef IMMX_BLK_NW
+#define IMMX_BLK_NW 8
+#endif
+constexpr int kBlkNW = IMMX_BLK_NW;
 constexpr int kBlkU = IMMX_BLK_U;
 
 // CTA shape per tier: the small tiers run 4 CTAs of 8 warps per SM; the large-hash and
@@ -1073,8 +1076,8 @@ uint32_t block_grid(Device& d, const Tier& tier, size_t smem) {
     constexpr int NW = BlkShape<KIND>::NW, U = BlkShape<KIND>::U;
     for (auto kern : {rrr_block_kernel<KIND, kProbGlobal, NW, U>, rrr_block_kernel<KIND, kProbRow, NW, U>,
                       rrr_block_kernel<KIND, kProbEdge, NW, U>}) {
-        if (smem > 48 * 1024)
-            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // (static + dynamic shared memory may pass 48 KB only with the attribute raised)
+        if (smem) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
     auto kern = rrr_block_kernel<KIND, kProbEdge, NW, U>;
