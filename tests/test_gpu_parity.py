@@ -87,8 +87,8 @@ def test_sample_duplicate_edges(im, orc):
 @pytest.mark.parametrize("p,lo,hi", [(0.006, 4096, 16384), (0.01, 16384, 1 << 30)])
 def test_sample_hash_tiers(im, orc, p, lo, hi):
     # n = 2^20 > 2^19: the visited set is a shared-memory hash (tier 1: 4,096 members);
-    # p near the giant-component threshold makes some sets restart on the 32-warp large-hash
-    # tier (<= 16,384 members, p = .006) or on the per-CTA global bitmap (p = .01)
+    # p near the giant-component threshold makes some sets grow past it: they continue in a
+    # promotion slot (the no-promotion restarts are covered below)
     g = im.generate_rmat(20, 8, 0.57, 0.19, 0.19, 11)
     im.assign_weights_f32(g, "uniform", p)
     gt = orc.transpose(csr_of(g))
@@ -97,6 +97,46 @@ def test_sample_hash_tiers(im, orc, p, lo, hi):
     assert_same_sets(a[0], a[1], b[0], b[1])
     sizes = np.diff(a[0].astype(np.int64))
     assert ((sizes > lo) & (sizes <= hi)).sum() >= 3
+
+
+def test_sample_beyond_promotion_slot(im, orc):
+    # p = 0.1 on n = 2^20: sets of ~164 K members outgrow a promotion slot's 2^17-member queue
+    # and finish on the per-CTA global-bitmap tier
+    g = im.generate_rmat(20, 8, 0.57, 0.19, 0.19, 11)
+    im.assign_weights_f32(g, "uniform", 0.1)
+    gt = orc.transpose(csr_of(g))
+    a = orc.sample_block(gt, 40, 0, 5)
+    b = sample_dev(im, gt, 40, 0, 5)
+    assert_same_sets(a[0], a[1], b[0], b[1])
+    assert (np.diff(a[0].astype(np.int64)) > (1 << 17)).sum() >= 3
+
+
+def test_sample_tiers_without_promotion(tmp_path):
+    # IMMX_NO_PROMOTE=1: overflowing samples restart on the 128 KB hash tier and the global
+    # bitmap instead of continuing in a slot (a separate process: the switch is read once)
+    import subprocess
+    import sys
+
+    code = (
+        "import sys; sys.path[:0] = ['tests', '.']\n"
+        "import numpy as np, paper_2208_00613_b200 as im\n"
+        "from oracle.oracle import Oracle\n"
+        "from conftest import csr_of\n"
+        "from test_gpu_parity import sample_dev, assert_same_sets\n"
+        "orc = Oracle()\n"
+        "g = im.generate_rmat(20, 8, 0.57, 0.19, 0.19, 11)\n"
+        "for p in (0.006, 0.01):\n"
+        "    im.assign_weights_f32(g, 'uniform', p)\n"
+        "    gt = orc.transpose(csr_of(g))\n"
+        "    a = orc.sample_block(gt, 600, 0, 5)\n"
+        "    b = sample_dev(im, gt, 600, 0, 5)\n"
+        "    assert_same_sets(a[0], a[1], b[0], b[1])\n"
+        "print('ok')\n")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IMMX_NO_PROMOTE="1")
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and p.stdout.strip().endswith("ok"), p.stderr[-2000:]
 
 
 def test_sample_rooted(im, orc):
