@@ -142,46 +142,39 @@ void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& l
     };
     std::vector<Job> jobs{{cb.root, root_bits, 0}};
     lut.assign((size_t)1 << root_bits, 0ULL);
+    // each table is filled by one walk of the subtree below its node, down to the table's
+    // width: a leaf at relative depth d covers 2^(width-d) consecutive entries; a node at the
+    // full width gets its own sub-table (each boundary node is reached by exactly one index);
+    // a missing child leaves its entries 0 (invalid).  Work ~ table entries + nodes.
+    struct Fr {
+        int32_t node;
+        uint32_t depth;
+        uint64_t prefix;
+    };
+    std::vector<Fr> st;
     while (!jobs.empty()) {
         const Job jb = jobs.back();
         jobs.pop_back();
-        const uint64_t entries = 1ULL << jb.width;
-        for (uint64_t x = 0; x < entries; ++x) {
-            int32_t u = jb.node;
-            uint32_t step = 0;
-            bool invalid = false;
-            while (step < jb.width) {
-                const auto& nd = cb.nodes[u];
-                if (nd.child[0] < 0 && nd.child[1] < 0) break;  // leaf
-                const uint32_t bit = (uint32_t)(x >> (jb.width - 1 - step)) & 1u;
-                const int32_t c = nd.child[bit];
-                if (c < 0) {
-                    invalid = true;
-                    break;
-                }
-                u = c;
-                ++step;
+        st.assign(1, {jb.node, 0, 0});
+        while (!st.empty()) {
+            const Fr f = st.back();
+            st.pop_back();
+            const auto& nd = cb.nodes[f.node];
+            if (nd.child[0] < 0 && nd.child[1] < 0) {
+                if (f.depth == 0) continue;  // only when the root itself is a leaf (cannot happen)
+                const unsigned long long e = (1ULL << 63) | ((unsigned long long)f.depth << 56) | nd.symbol;
+                const uint64_t span = 1ULL << (jb.width - f.depth);
+                std::fill(lut.begin() + jb.offset + f.prefix * span, lut.begin() + jb.offset + (f.prefix + 1) * span, e);
+            } else if (f.depth == jb.width) {
+                const uint32_t w = std::max<uint32_t>(1, std::min<uint32_t>(8, height[f.node]));
+                const uint64_t off = lut.size();
+                lut.resize(off + (1ULL << w), 0ULL);
+                jobs.push_back({f.node, w, off});
+                lut[jb.offset + f.prefix] = (1ULL << 62) | ((unsigned long long)w << 56) | off;
+            } else {
+                for (int c = 1; c >= 0; --c)
+                    if (nd.child[c] >= 0) st.push_back({nd.child[c], f.depth + 1, f.prefix * 2 + (uint64_t)c});
             }
-            unsigned long long e = 0;
-            if (!invalid) {
-                const auto& nd = cb.nodes[u];
-                if (nd.child[0] < 0 && nd.child[1] < 0) {
-                    if (step == 0) {
-                        invalid = true;  // only when the root itself is a leaf (cannot happen)
-                    } else {
-                        e = (1ULL << 63) | ((unsigned long long)step << 56) | nd.symbol;
-                    }
-                } else {
-                    // internal node after `width` bits: pointer to its own sub-table (each
-                    // boundary node is reached by exactly one index, so no sharing is needed)
-                    const uint32_t w = std::max<uint32_t>(1, std::min<uint32_t>(8, height[u]));
-                    const uint64_t off = lut.size();
-                    lut.resize(off + (1ULL << w), 0ULL);
-                    jobs.push_back({u, w, off});
-                    e = (1ULL << 62) | ((unsigned long long)w << 56) | off;
-                }
-            }
-            lut[jb.offset + x] = invalid ? 0ULL : e;
         }
     }
 }

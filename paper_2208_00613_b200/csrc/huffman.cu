@@ -697,6 +697,43 @@ __global__ void k_raw_mark(const RawChunkView* __restrict__ chunks, uint32_t nch
     warp_add_u64(&ctl->hvol, hv);
 }
 
+// find by scanning the raw sets (warp per set, stop at the pick): round 0 on inputs whose
+// first pick covers most of the volume, and every round when the live sets are few
+__global__ void k_raw_scan_mark(const uint32_t* __restrict__ arena, const uint64_t* __restrict__ off,
+                                const uint32_t* __restrict__ len, uint64_t count, RoundCtl* ctl,
+                                uint32_t* __restrict__ covered, uint32_t r, uint32_t* __restrict__ hitlist,
+                                unsigned int* __restrict__ hist0, unsigned int* __restrict__ hist1, uint64_t n) {
+    const uint32_t pick = ctl->pick;
+    if (pick == 0xffffffffu) return;
+    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gs = (uint64_t)gridDim.x * blockDim.x;
+    {
+        const uint32_t cur = ctl->cur;
+        unsigned int* spare = cur ? hist0 : hist1;
+        for (uint64_t v = gt; v < n; v += gs) spare[v] = 0;
+        if (gt == 0) {
+            ctl->cur_snap = cur;
+            ctl->live_snap = ctl->live_vol;
+        }
+    }
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = gt >> 5, nw = gs >> 5;
+    unsigned long long hv = 0;
+    for (uint64_t j = w; j < count; j += nw) {
+        if (covered[j]) continue;
+        const uint64_t b = off[j];
+        const uint32_t l = len[j];
+        bool found = false;
+        for (uint32_t i0 = 0; i0 < l && !found; i0 += 32)
+            found = __any_sync(FULL, i0 + lane < l && arena[b + i0 + lane] == pick);
+        if (found && lane == 0) {
+            covered[j] = r + 1;
+            hitlist[atomicAdd(&ctl->nhit, 1ull)] = (uint32_t)j;
+            hv += l;
+        }
+    }
+    warp_add_u64(&ctl->hvol, hv);
+}
+
 // apply: subtract the hits' members (warp per hit) or recount the live sets (warp per set)
 __global__ void k_raw_apply(const uint32_t* __restrict__ arena, const uint64_t* __restrict__ off,
                             const uint32_t* __restrict__ len, uint64_t count, RoundCtl* ctl,
@@ -1189,26 +1226,31 @@ void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
     if (theta == 0) fail(IMMX_EINVAL, "selection requires at least one set");
     if (k >= n) fail(IMMX_EINVAL, "selection requires k < n");
     if (theta >= 0xffffffffULL) fail(IMMX_EINVAL, "more than 2^32-1 sets");
-    // the index: reuse the chunks of earlier calls on this pool, add one for the new sets
+    // running table over the pool (only the new sets are counted) and, when it pays, an
+    // inverted index of chunks (one per call that needed it; earlier chunks are reused)
     Pool& Pm = const_cast<Pool&>(P);
     if (!Pm.rix) Pm.rix = std::make_shared<RawIndex>();
     RawIndex& X = *Pm.rix;
-    if (X.epoch != P.epoch || X.n != n || X.indexed > theta) {
+    if (X.epoch != P.epoch || X.n != n || X.hist_upto > theta || X.indexed > theta) {
         X.chunks.clear();
-        X.indexed = 0;
+        X.indexed = X.hist_upto = X.indexed_members = 0;
         X.epoch = P.epoch;
         X.n = n;
         X.hist.exact(n);
         CK(cudaMemsetAsync(X.hist.p, 0, n * 4, s));
     }
-    if (X.indexed < theta) {
+    if (X.hist_upto < theta) {
+        pool_hist_dev(P, X.hist_upto, theta, X.hist.p);
+        X.hist_upto = theta;
+    }
+    auto build_index = [&]() {
+        if (X.indexed >= theta) return;
         const uint64_t lo = X.indexed, hi = theta;
         auto ch = std::make_unique<RawIndex::Chunk>();
         DBuf<unsigned int> cnt;
         cnt.exact(n);
         CK(cudaMemsetAsync(cnt.p, 0, n * 4, s));
         pool_hist_dev(P, lo, hi, cnt.p);
-        k_add_u32<<<grid_for(n, d), 256, 0, s>>>(X.hist.p, cnt.p, n);
         DBuf<uint64_t> c64;
         c64.exact(n + 1);
         CK(cudaMemsetAsync(c64.p, 0, 8, s));
@@ -1231,13 +1273,13 @@ void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
         d.kernel_launches += 3;
         X.chunks.push_back(std::move(ch));
         X.indexed = theta;
+        X.indexed_members += tot;
         std::vector<RawChunkView> views;
         for (auto& c : X.chunks) views.push_back({c->off.p, c->idx.p});
         X.meta.exact((views.size() * sizeof(RawChunkView) + 7) / 8);
         CK(cudaMemcpyAsync(X.meta.p, views.data(), views.size() * sizeof(RawChunkView), cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
-    }
-    const uint32_t nch = (uint32_t)X.chunks.size();
+    };
     DBuf<unsigned int>& hist = d.ws_hist;  // the working table (+ its double)
     hist.exact(2 * n);
     CK(cudaMemcpyAsync(hist.p, X.hist.p, n * 4, cudaMemcpyDeviceToDevice, s));
@@ -1261,12 +1303,28 @@ void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
         CK(cudaMemcpyAsync(ctl, &h, sizeof(h), cudaMemcpyHostToDevice, s));
     }
     const unsigned grid_am = grid_for(n, d), grid_w = (unsigned)d.num_sms * 8;
-    const RawChunkView* views = reinterpret_cast<const RawChunkView*>(X.meta.p);
+    // round 0 scans the sets; afterwards the index is used unless scanning the live volume
+    // for the remaining rounds is cheaper than indexing the unindexed members
+    bool scan = true;
     std::vector<KTimer> kt(k);
     for (uint32_t r = 0; r < k; ++r) {
+        if (r == 1) {
+            unsigned long long live = 0;
+            CK(cudaMemcpyAsync(&live, &ctl->live_vol, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            const uint64_t unindexed = P.members - X.indexed_members;
+            scan = (uint64_t)live * (k - 1) < 4 * unindexed;
+            if (!scan) build_index();
+        }
         k_argmax_pick<<<grid_am, 256, 0, s>>>(hist.p, hist.p + n, n, ctl, keys.p, r, is_seed.p, seeds.p, marg.p);
         kt[r].start(&d, IMMX_KSTAT_RSELECT);
-        k_raw_mark<<<grid_w, 256, 0, s>>>(views, nch, ctl, covered.p, P.len.p, r, hitlist.p, hist.p, hist.p + n, n);
+        if (scan)
+            k_raw_scan_mark<<<grid_w, 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, theta, ctl, covered.p, r, hitlist.p,
+                                                   hist.p, hist.p + n, n);
+        else
+            k_raw_mark<<<grid_w, 256, 0, s>>>(reinterpret_cast<const RawChunkView*>(X.meta.p),
+                                              (uint32_t)X.chunks.size(), ctl, covered.p, P.len.p, r, hitlist.p, hist.p,
+                                              hist.p + n, n);
         k_raw_apply<<<grid_w, 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, theta, ctl, covered.p, hitlist.p, hist.p,
                                            hist.p + n, n);
         kt[r].stop();

@@ -145,8 +145,8 @@ struct DevGraph {
 // appends sets, so each call indexes just the new ones (one chunk per call) and keeps a
 // running vertex histogram
 struct RawIndex {
-    uint64_t epoch = ~0ULL, n = 0, indexed = 0;
-    DBuf<unsigned int> hist;  // counts over sets [0, indexed)
+    uint64_t epoch = ~0ULL, n = 0, indexed = 0, hist_upto = 0, indexed_members = 0;
+    DBuf<unsigned int> hist;  // counts over sets [0, hist_upto)
     struct Chunk {
         DBuf<uint64_t> off;   // n+1 offsets into idx
         DBuf<uint32_t> idx;   // set ids, grouped by vertex
