@@ -1,0 +1,65 @@
+// huffman_dev.cuh -- device-side reading of the Huffman store: the bit reader and the
+// multi-level decode-table lookup (entry layout: huffman.cu header).  Shared by
+// huffman.cu (decode_find) and select.cu (select_huffman).
+#pragma once
+
+#include <cstdint>
+
+namespace immx_dev {
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+
+// ---- bit reader over one set's stream -------------------------------------------
+struct BitReader {
+    const uint32_t* w;
+    uint64_t buf;
+    uint32_t nb;     // valid bits in buf (MSB-aligned)
+    uint32_t next;   // next word to load
+    __device__ void init(const uint32_t* words) {
+        w = words;
+        buf = 0;
+        nb = 0;
+        next = 0;
+        refill();
+        refill();
+    }
+    __device__ __forceinline__ void refill() {
+        if (nb <= 32) {
+            buf |= (uint64_t)bswap32(__ldg(w + next)) << (32 - nb);
+            nb += 32;
+            next++;
+        }
+    }
+    __device__ __forceinline__ uint32_t peek(uint32_t W) const { return (uint32_t)(buf >> (64 - W)); }
+    __device__ __forceinline__ void skip(uint32_t L) {
+        buf = L == 64 ? 0 : (buf << L);
+        nb -= L;
+        refill();
+    }
+};
+
+// decode one codeword; returns symbol, sets consumed bits; invalid -> false
+__device__ __forceinline__ bool decode_one(BitReader& br, const unsigned long long* __restrict__ lut, uint32_t root_bits,
+                                           uint32_t& sym, uint32_t& used) {
+    uint64_t toff = 0;
+    uint32_t W = root_bits;
+    used = 0;
+    for (;;) {
+        const unsigned long long e = __ldg(lut + toff + br.peek(W));
+        if (e >> 63) {
+            const uint32_t L = (uint32_t)(e >> 56) & 0x7f;
+            br.skip(L);
+            used += L;
+            sym = (uint32_t)e;
+            return true;
+        }
+        if (!((e >> 62) & 1)) return false;
+        br.skip(W);
+        used += W;
+        W = (uint32_t)(e >> 56) & 0x3f;
+        toff = e & 0xffffffffffffULL;
+    }
+}
+
+}  // namespace immx_dev
