@@ -313,12 +313,26 @@ def run_ours(args, cfg, rank, world, local):
     # DRAM bytes per launch: the dram/algorithmic ratio of the ncu --set full capture of the
     # same kernel on this config (profiles/), applied to this run's bytes per launch
     traffic = None
+    issue = None
     prof = os.path.join(ROOT, "profiles", "ncu_sampler_traffic.json")
+    clocks = clk.summary()
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                ratio = json.load(f)[args.config]["dram_over_alg"]
-            traffic = ratio * samp["bytes"] / max(samp["launches"], 1)
+                pc = json.load(f)[args.config]
+            traffic = pc["dram_over_alg"] * samp["bytes"] / max(samp["launches"], 1)
+            # the sampler's real bound: instruction issue (ALU-heavy integer work on an
+            # L2-resident graph).  warp-instructions per edge from the ncu capture x the live
+            # edge rate of the kernel, against 4 issue slots per SM per clock
+            edges = sum(x["edges_scanned"] for x in results)
+            eps = edges / (samp["ms"] / 1000.0) if samp["ms"] else None
+            sm_mhz = clocks.get("sm_mhz") or 1965.0
+            if eps and "warp_inst_per_edge" in pc:
+                ach = eps * pc["warp_inst_per_edge"]
+                pk = 4 * torch.cuda.get_device_properties(local).multi_processor_count * sm_mhz * 1e6
+                issue = {"bound": "issue", "achieved": ach, "peak": pk, "unit": "warp-inst/s", "frac": ach / pk,
+                         "warp_inst_per_edge": pc["warp_inst_per_edge"], "edges_per_s": eps,
+                         "source": "profiles/ncu_sampler_traffic.json (ncu instruction count of the same kernel)"}
         except Exception:
             traffic = None
 
@@ -332,7 +346,6 @@ def run_ours(args, cfg, rank, world, local):
                              f"{dt:.1f} s on {threads} host threads"}
         except Exception as ex:  # reference build missing on this box
             cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
-    clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -347,10 +360,12 @@ def run_ours(args, cfg, rank, world, local):
         "phase_seconds": r0["phase_seconds"],
         "seeds_head": r0["seeds"][:5],
         "roofline": {"bound": "hbm", "achieved": samp_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": (samp_gbs / peak) if samp_gbs else None, "traffic": traffic, "kernel": "rrr_kernel",
+                     "frac": (samp_gbs / peak) if samp_gbs else None, "traffic": traffic,
+                     "kernel": "rrr_block_kernel (sampler)",
                      "peak_kind": peak_kind, "launches": samp["launches"],
                      "alg_bytes_per_launch": samp["bytes"] / max(samp["launches"], 1),
                      "avg_launch_ms": samp["ms"] / max(samp["launches"], 1)},
+        "roofline_issue": issue,
         "select_roofline": {"achieved": hsel["bytes"] / (hsel["ms"] / 1000) / 1e9 if hsel["ms"] else None,
                             "unit": "GB/s", "launches": hsel["launches"], "ms": hsel["ms"]},
         "encode_roofline": {"achieved": enc["bytes"] / (enc["ms"] / 1000) / 1e9 if enc["ms"] else None,
