@@ -539,7 +539,6 @@ struct BlkSmem {
     alignas(16) uint32_t wsum[NW];
     alignas(16) uint32_t wsum2[NW];
     uint32_t nextrow[2][NW];  // rows of the next group's warp starts (double-buffered)
-    uint32_t nextpos[2];      // the gpos those rows were computed for
     uint32_t hdup;            // hash tiers: duplicate keys left by conflict rollbacks
     int pslot;                // hash tiers: the promotion slot taken (-1: none)
     uint32_t lpos[NW * 32 * U];  // rare path: success positions
@@ -578,18 +577,12 @@ __device__ __forceinline__ uint32_t advance_row(const uint32_t* cum, uint32_t r,
 // sum of the first `w` entries and of all NW entries of a per-warp smem array
 template <int NW>
 __device__ __forceinline__ void warp_prefix(const uint32_t* a, uint32_t w, uint32_t& before, uint32_t& total) {
-    // lanes 0..NW-1 load one entry each and scan with shuffles (called by full warps)
+    // lanes 0..NW-1 load one entry each; two warp reductions (called by full warps)
     static_assert(NW <= 32, "NW must fit a warp");
     const uint32_t lane = lane_id();
-    uint32_t x = lane < (uint32_t)NW ? a[lane] : 0u;
-#pragma unroll
-    for (int o = 1; o < NW; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= (uint32_t)o) x += y;
-    }
-    total = __shfl_sync(0xffffffffu, x, NW - 1);
-    before = __shfl_sync(0xffffffffu, x, (w + NW - 1) % NW);
-    if (w == 0) before = 0;
+    const uint32_t x = lane < (uint32_t)NW ? a[lane] : 0u;
+    total = __reduce_add_sync(0xffffffffu, x);
+    before = __reduce_add_sync(0xffffffffu, lane < w ? x : 0u);
 }
 
 template <int KIND, int PM, int NW, int U>
@@ -713,7 +706,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
                 uint32_t gpos = 0;
                 uint32_t r_w = 0;  // row holding this warp's first position (monotone over the batch)
                 uint32_t par = 0;  // group parity (double buffer of the precomputed start rows)
-                if (tid < 2) sh.nextpos[tid] = 0xffffffffu;
+                bool pre_ok = false;  // warp 0 precomputed this group's warp-start rows (no cut since)
                 __syncthreads();
                 while (gpos < total) {
                     // ---- one group: positions gpos + (w*U + i)*32 + lane ----
@@ -724,14 +717,13 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
                     uint32_t wd = 0;
                     const uint32_t a0 = gpos + w * U * 32;
                     const uint32_t a0c = min(a0, total - 1);
-                    if (sh.nextpos[par] == gpos && a0 < total) r_w = sh.nextrow[par][w];  // precomputed
+                    if (pre_ok && a0 < total) r_w = sh.nextrow[par][w];  // precomputed by warp 0
                     else r_w = advance_row<NW>(sh.cum, r_w, a0c);
                     if (w == 0) {
                         // the next group's warp starts (valid unless a conflict cut moves gpos):
                         // NW parallel searches in lanes 0..NW-1, published by this group's barriers
                         const uint32_t x = gpos + G + lane * U * 32;
                         if (lane < (uint32_t)NW && x < total) sh.nextrow[par ^ 1][lane] = advance_row<NW>(sh.cum, r_w, x);
-                        if (lane == 0) sh.nextpos[par ^ 1] = gpos + G;
                     }
                     // this warp's slice leaves the row holding gpos -> the group spans several rows
                     bool my_multi = false;
@@ -842,6 +834,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
                         qlen += stotal;
                         t += dtotal;
                         gpos += G;
+                        pre_ok = true;
                         par ^= 1;
                     } else {
                         // rare: resolve the first position whose target repeats an earlier success
@@ -955,7 +948,8 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
                               }
                             }
                         }
-                        gpos = cut == 0xffffffffu ? gpos + G : cut;
+                        pre_ok = cut == 0xffffffffu;
+                        gpos = pre_ok ? gpos + G : cut;
                         par ^= 1;
                         __syncthreads();  // rare path: rebuilt visited set, smem success list reuse
                     }
