@@ -361,7 +361,7 @@ def run_ours(args, cfg, rank, world, local):
         "seeds_head": r0["seeds"][:5],
         "roofline": {"bound": "hbm", "achieved": samp_gbs, "peak": peak, "unit": "GB/s",
                      "frac": (samp_gbs / peak) if samp_gbs else None, "traffic": traffic,
-                     "kernel": "rrr_block_kernel (sampler)",
+                     "kernel": "rrr_kernel (LT walks)" if "lt_seed" in cfg else "rrr_block_kernel (IC sampler)",
                      "peak_kind": peak_kind, "launches": samp["launches"],
                      "alg_bytes_per_launch": samp["bytes"] / max(samp["launches"], 1),
                      "avg_launch_ms": samp["ms"] / max(samp["launches"], 1)},

@@ -115,6 +115,7 @@ struct SampleResult {
     uint32_t size;    // members written to q
     uint64_t edges;   // edges of the members' rows (E_j)
     bool overflow;
+    uint64_t probes = 0;  // LT: cumulative-weight entries read by the searches
 };
 
 template <int U, class Vis>
@@ -270,7 +271,7 @@ __device__ __forceinline__ SampleResult walk_lt(const GView& g, Vis& vis, uint32
                                 uint32_t root, uint64_t s0, uint64_t t) {
     const uint32_t lane = lane_id();
     uint32_t qlen = 1;
-    uint64_t edges = 0;
+    uint64_t edges = 0, probes = 0;
     if (lane == 0) {
         q[0] = root;
         vis.add(root);
@@ -282,25 +283,34 @@ __device__ __forceinline__ SampleResult walk_lt(const GView& g, Vis& vis, uint32
         if (b == e) break;
         const double r = (double)(draw(s0, t) >> 11) * 0x1.0p-53;
         t++;
-        // first index with r < cum: warp-parallel search over 32-wide chunks
-        int64_t chosen = -1;
-        for (uint64_t base = b; base < e; base += 32) {
-            const uint64_t idx = base + lane;
-            const bool hit = idx < e && r < g.lt_cum[idx];
-            const uint32_t hm = __ballot_sync(FULL, hit);
-            if (hm) {
-                chosen = (int64_t)(base + __ffs(hm) - 1);
-                edges += (uint64_t)(chosen - b + 1);
-                break;
-            }
-        }
-        if (chosen < 0) {
+        // first index with r < cum (cum is non-decreasing along the row): a 32-ary search --
+        // each step probes 32 evenly spaced entries and keeps the sub-range before the first
+        // hit -- then one 32-wide scan; log32(deg) steps instead of deg/32 on hub rows.  The
+        // edge count is the reference walk's (oc_sample_lt): position of the choice + 1.
+        probes += 1;
+        if (!(r < __ldg(g.lt_cum + e - 1))) {  // r >= the row's total weight: no choice
             edges += e - b;
             break;
         }
+        uint64_t lo = b, hi = e;  // the choice lies in [lo, hi)
+        while (hi - lo > 32) {
+            const uint64_t step = (hi - lo + 31) / 32;
+            const uint64_t p = min(lo + (lane + 1) * step, hi) - 1;
+            const uint32_t hm = __ballot_sync(FULL, r < __ldg(g.lt_cum + p));  // lane 31 (p = hi-1) hits
+            probes += 32;
+            const uint32_t f = __ffs(hm) - 1;
+            const uint64_t nlo = lo + (uint64_t)f * step;
+            hi = min(lo + (uint64_t)(f + 1) * step, hi);
+            lo = nlo;
+        }
+        const uint64_t idx = lo + lane;
+        const uint32_t hm = __ballot_sync(FULL, idx < hi && r < __ldg(g.lt_cum + idx));
+        const int64_t chosen = (int64_t)(lo + __ffs(hm) - 1);
+        edges += (uint64_t)(chosen - b + 1);
+        probes += hi - lo;
         const uint32_t v = g.col[chosen];
         if (vis.has(v)) break;
-        if (qlen + 1 > qcap) return {qlen, edges, true};
+        if (qlen + 1 > qcap) return {qlen, edges, true, probes};
         __syncwarp();
         if (lane == 0) {
             q[qlen] = v;
@@ -310,7 +320,7 @@ __device__ __forceinline__ SampleResult walk_lt(const GView& g, Vis& vis, uint32
         qlen++;
         cur = v;
     }
-    return {qlen, edges, false};
+    return {qlen, edges, false, probes};
 }
 
 // ------------------------------------------------------------------ the kernel ----
@@ -323,6 +333,7 @@ struct SampCtl {
     unsigned long long members;
     unsigned long long edges_abandoned;  // scanned by samples that moved to the next tier
     unsigned long long n_promoted;       // samples that continued in a promotion slot
+    unsigned long long probes;           // LT: cumulative-weight entries read
 };
 
 struct SampJob {
@@ -430,6 +441,7 @@ __global__ void __launch_bounds__(256) rrr_kernel(GView g, SampJob job, uint32_t
                     job.set_len[job.pool_base + j] = res.size;
                     atomicAdd(&job.ctl->edges, (unsigned long long)res.edges);
                     atomicAdd(&job.ctl->members, (unsigned long long)res.size);
+                    if (res.probes) atomicAdd(&job.ctl->probes, (unsigned long long)res.probes);
                 }
             }
         } else if (lane == 0) {
@@ -1326,7 +1338,12 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
             // algorithmic bytes of the samples this launch committed
             const uint64_t committed = nitems - n_ovf - n_nospace;
             const bool edge_bytes = G.pmode == kProbEdge || model == IMMX_MODEL_LT;
-            kt.finish(12ULL * hctl->members + 4ULL * hctl->edges * (edge_bytes ? 2 : 1) + 8ULL * committed);
+            // LT walks read only the cumulative weights their searches probe (8 B each) plus
+            // the chosen neighbour id, not every edge of the row
+            const uint64_t edge_part = model == IMMX_MODEL_LT
+                                           ? 8ULL * hctl->probes + 4ULL * hctl->members
+                                           : 4ULL * hctl->edges * (edge_bytes ? 2 : 1);
+            kt.finish(12ULL * hctl->members + edge_part + 8ULL * committed);
         }
         if (n_nospace) {
             // grow the arena past everything reserved so far and redo those samples here
