@@ -7,6 +7,8 @@
 // scalar control (theta arithmetic sampler.cpp:54-83, characterization characterize.cpp,
 // the Huffman tree huffman.cpp:24-84, the memory ledger memory.hpp) on the host.
 #include <cub/cub.cuh>
+#include <cstdio>
+#include <cstdlib>
 
 #include <chrono>
 #include <memory>
@@ -915,8 +917,12 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     const auto tc = Clock::now();
                     std::vector<unsigned long long> leaves;
                     codebook_leaves_dev(d, h1.p, n, leaves);
+                    const double t_leaves = secs(tc);
                     cb = build_codebook_sorted(leaves.data(), leaves.size(), n);
                     t_codebook = secs(tc);
+                    if (std::getenv("IMMX_DEBUG_CODEBOOK"))
+                        std::fprintf(stderr, "[immx codebook] coded %llu leaves (device sort + D2H) %.4f s, tree+codes %.4f s\n",
+                                     (unsigned long long)leaves.size(), t_leaves, t_codebook - t_leaves);
                     const auto tl = Clock::now();
                     std::vector<unsigned long long> lut;
                     uint32_t rb = 1;
@@ -928,7 +934,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     store->s.dense_count = 0;
                     store->s.n_extra = 0;
                     store->s.hybrid = mode == IMMX_MODE_HYBRID;
-                    store_set_codes(store->s, d, n, cb.bits.data(), cb.len.data(), lut, rb);
+                    store_set_leaf_codes(store->s, d, n, cb, lut, rb);
                 } else if (mode == IMMX_MODE_BITMAP) {
                     bm.reset(new immx_bitmap);
                     bm->b.dev = &d;
@@ -970,13 +976,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         const double ratio = enc_total == 0 ? 1.0 : (double)raw_total / (double)enc_total;
         double uncoded = 0.0;
         if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {
-            std::vector<unsigned int> hh(n);
-            CK(cudaMemcpyAsync(hh.data(), hist.p, n * 4, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            uint64_t u = 0;
-            for (uint64_t v = 0; v < n; ++v)
-                if (hh[v] > 0 && cb.len[v] == 0) u++;
-            uncoded = (double)u / (double)n;
+            uncoded = (double)count_uncoded_dev(d, hist.p, store->s.code_len.p, n) / (double)n;
         }
 
         // ---- selection (pipeline.cpp:156-175) ----

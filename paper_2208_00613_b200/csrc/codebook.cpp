@@ -23,10 +23,12 @@ namespace {
 // once each equal-frequency run of merged nodes is ordered by min id at its first use.
 // Linear after the leaf sort, which the device does (codebook_leaves_dev).
 template <class F, class I>
-HostCodebook merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id) {
+HostCodebook merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id, bool per_vertex) {
     HostCodebook cb;
-    cb.bits.assign(n, 0);
-    cb.len.assign(n, 0);
+    if (per_vertex) {
+        cb.bits.assign(n, 0);
+        cb.len.assign(n, 0);
+    }
     cb.children_first = true;
     if (!L) fail(IMMX_ERUNTIME, "cannot build a codebook from an empty block");
     if (L >= (1ULL << 31)) fail(IMMX_EINVAL, "too many coded symbols");
@@ -36,8 +38,14 @@ HostCodebook merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id) {
     if (L == 1) {
         cb.nodes[1].child[0] = 0;
         cb.root = 1;
-        cb.bits[leaf_id(0)] = 0;  // a single symbol gets the 1-bit code "0"
-        cb.len[leaf_id(0)] = 1;
+        // a single symbol gets the 1-bit code "0"
+        cb.leaf_sym.assign(1, leaf_id(0));
+        cb.leaf_bits.assign(1, 0);
+        cb.leaf_len.assign(1, 1);
+        if (per_vertex) {
+            cb.bits[leaf_id(0)] = 0;
+            cb.len[leaf_id(0)] = 1;
+        }
         return cb;
     }
     struct Q {
@@ -92,19 +100,24 @@ HostCodebook merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id) {
             dep[ch] = (uint8_t)(dep[u] + 1);
         }
     }
-    for (uint64_t i = 0; i < L; ++i) {
-        cb.bits[cb.nodes[i].symbol] = pre[i];
-        cb.len[cb.nodes[i].symbol] = dep[i];
-    }
+    cb.leaf_sym.resize(L);
+    cb.leaf_bits.assign(pre.begin(), pre.begin() + L);
+    cb.leaf_len.assign(dep.begin(), dep.begin() + L);
+    for (uint64_t i = 0; i < L; ++i) cb.leaf_sym[i] = cb.nodes[i].symbol;
+    if (per_vertex)
+        for (uint64_t i = 0; i < L; ++i) {
+            cb.bits[cb.nodes[i].symbol] = pre[i];
+            cb.len[cb.nodes[i].symbol] = dep[i];
+        }
     return cb;
 }
 
 }  // namespace
 
-HostCodebook build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n) {
+HostCodebook build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n, bool per_vertex) {
     return merge_sorted(
         count, n, [&](uint64_t i) { return (uint64_t)(leaves[i] >> 32); },
-        [&](uint64_t i) { return (uint32_t)(leaves[i] & 0xffffffffu); });
+        [&](uint64_t i) { return (uint32_t)(leaves[i] & 0xffffffffu); }, per_vertex);
 }
 
 HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n) {
@@ -113,7 +126,7 @@ HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n) {
         if (freq[v]) ids.push_back((uint32_t)v);
     std::stable_sort(ids.begin(), ids.end(), [&](uint32_t a, uint32_t b) { return freq[a] < freq[b]; });
     return merge_sorted(
-        ids.size(), n, [&](uint64_t i) { return freq[ids[i]]; }, [&](uint64_t i) { return ids[i]; });
+        ids.size(), n, [&](uint64_t i) { return freq[ids[i]]; }, [&](uint64_t i) { return ids[i]; }, true);
 }
 
 // Multi-level decode table (entry layout: huffman.cu header).  Table widths: root

@@ -217,6 +217,24 @@ __global__ void k_decode_find(const uint32_t* __restrict__ words, uint64_t woff,
     out[0] = 0;
 }
 
+__global__ void k_scatter_codes(const uint32_t* __restrict__ sym, const uint64_t* __restrict__ bits,
+                                const uint8_t* __restrict__ len, uint64_t L, uint64_t* __restrict__ code_bits,
+                                uint8_t* __restrict__ code_len) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < L; i += (uint64_t)gridDim.x * blockDim.x) {
+        code_bits[sym[i]] = bits[i];
+        code_len[sym[i]] = len[i];
+    }
+}
+
+__global__ void k_count_uncoded(const unsigned int* __restrict__ hist, const uint8_t* __restrict__ code_len, uint64_t n,
+                                unsigned long long* __restrict__ out) {
+    unsigned long long c = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+        c += hist[v] > 0 && code_len[v] == 0;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 __global__ void k_seg_flags(const uint64_t* __restrict__ nx, const uint64_t* __restrict__ xoff, uint64_t cnt,
                             uint64_t xbase, uint8_t* __restrict__ segd, uint32_t* __restrict__ xfirst) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -233,6 +251,55 @@ __global__ void k_add2(uint64_t* __restrict__ a, uint64_t* __restrict__ b, uint6
 }
 
 }  // namespace
+
+void store_set_leaf_codes(Store& S, Device& d, uint64_t n, const HostCodebook& cb,
+                          const std::vector<unsigned long long>& lut, uint32_t root_bits) {
+    cudaStream_t s = d.stream;
+    S.dev = &d;
+    S.n = n;
+    S.code_bits.exact(std::max<uint64_t>(n, 1));
+    S.code_len.exact(std::max<uint64_t>(n, 1));
+    CK(cudaMemsetAsync(S.code_len.p, 0, n, s));
+    const uint64_t L = cb.leaf_sym.size();
+    if (L) {
+        DBuf<uint32_t> sym;
+        DBuf<uint64_t> bits;
+        DBuf<uint8_t> len;
+        sym.exact(L);
+        bits.exact(L);
+        len.exact(L);
+        CK(cudaMemcpyAsync(sym.p, cb.leaf_sym.data(), L * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(bits.p, cb.leaf_bits.data(), L * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(len.p, cb.leaf_len.data(), L, cudaMemcpyHostToDevice, s));
+        k_scatter_codes<<<grid_for(L, d), 256, 0, s>>>(sym.p, bits.p, len.p, L, S.code_bits.p, S.code_len.p);
+        CK_LAUNCH("k_scatter_codes");
+        d.kernel_launches++;
+        CK(cudaStreamSynchronize(s));  // the leaf buffers go out of scope
+    }
+    S.lut.exact(std::max<uint64_t>(lut.size(), 1));
+    if (!lut.empty()) CK(cudaMemcpyAsync(S.lut.p, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice, s));
+    S.lut_root_bits = root_bits;
+    S.lut_entries = lut.size();
+    S.woff.reserve(1, s);
+    S.coff.reserve(1, s);
+    uint64_t z = 0;
+    CK(cudaMemcpyAsync(S.woff.p, &z, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(S.coff.p, &z, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+uint64_t count_uncoded_dev(Device& d, const unsigned int* d_hist, const uint8_t* d_code_len, uint64_t n) {
+    cudaStream_t s = d.stream;
+    unsigned long long* out = d.scal.p + 28;
+    CK(cudaMemsetAsync(out, 0, 8, s));
+    k_count_uncoded<<<grid_for(n, d), 256, 0, s>>>(d_hist, d_code_len, n, out);
+    CK_LAUNCH("k_count_uncoded");
+    d.kernel_launches++;
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, out, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return h;
+}
 
 void store_set_codes(Store& S, Device& d, uint64_t n, const uint64_t* code_bits, const uint8_t* code_len,
                      const std::vector<unsigned long long>& lut, uint32_t root_bits) {

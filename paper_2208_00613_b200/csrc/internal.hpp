@@ -246,6 +246,12 @@ void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out);
 void pool_read_host(const Pool& P, uint64_t lo, uint64_t hi, uint64_t* offsets, uint32_t* members);
 void pool_upload_host(Pool& P, const uint64_t* offsets, const uint32_t* members, uint64_t count, uint64_t n_check);
 // huffman.cu
+struct HostCodebook;
+// the codes of the coded vertices only (scattered on the device; every other vertex uncoded)
+void store_set_leaf_codes(Store& S, Device& d, uint64_t n, const HostCodebook& cb,
+                          const std::vector<unsigned long long>& lut, uint32_t root_bits);
+// vertices counted in the table (hist > 0) that have no code
+uint64_t count_uncoded_dev(Device& d, const unsigned int* d_hist, const uint8_t* d_code_len, uint64_t n);
 void store_set_codes(Store& S, Device& d, uint64_t n, const uint64_t* code_bits, const uint8_t* code_len,
                      const std::vector<unsigned long long>& lut, uint32_t root_bits);
 void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top, uint64_t* payload_out);
@@ -320,8 +326,11 @@ struct HostCodebook {
         int32_t child[2] = {-1, -1};
         uint32_t symbol = 0;
     };
-    std::vector<uint64_t> bits;
+    std::vector<uint64_t> bits;  // per vertex (n entries) -- only when built with per_vertex
     std::vector<uint8_t> len;
+    std::vector<uint32_t> leaf_sym;   // per coded vertex (the Huffman merge's leaf order)
+    std::vector<uint64_t> leaf_bits;
+    std::vector<uint8_t> leaf_len;
     std::vector<Node> nodes;
     int32_t root = 0;
     bool children_first = false;  // true: every child index < its parent's (Huffman merge order)
@@ -329,7 +338,8 @@ struct HostCodebook {
 };
 HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n);
 // leaves = the coded vertices as (freq << 32 | id), sorted ascending
-HostCodebook build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n);
+HostCodebook build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n,
+                                   bool per_vertex = false);
 void codebook_leaves_dev(Device& d, const unsigned int* d_hist, uint64_t n, std::vector<unsigned long long>& leaves);
 void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& lut, uint32_t& root_bits);
 
