@@ -545,7 +545,7 @@ struct BVisOf<kBGlob> { using T = BGBits; };
 
 template <int NW, int U>
 struct BlkSmem {
-    uint64_t rs[NW * 32];    // col index of flattened position 0 of the row (row start - exclusive cum)
+    const uint32_t* rs[NW * 32];  // &col[flattened position 0 of the row] (row start - exclusive cum)
     uint32_t cum[NW * 32];   // inclusive prefix of the batch's row degrees
     uint64_t thr[NW * 32];   // row threshold (global / per-row modes)
     alignas(16) uint32_t wsum[NW];
@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
                 if (deg > 0) {
                     const uint32_t c = coff + __popc(nem & lt);
                     sh.cum[c] = x + off;
-                    sh.rs[c] = rs - (uint64_t)(x + off - deg);  // col index of flattened position p = rs + p
+                    sh.rs[c] = g.col + (rs - (uint64_t)(x + off - deg));  // position p's target: rs[c][p]
                     if (PM == kProbRow) sh.thr[c] = th;
                 }
                 if (tid >= nrows) sh.cum[tid] = total;
@@ -742,14 +742,13 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
                     if (a0 < total && sh.cum[r_w] >= min(a0 + U * 32, total)) {
                         my_multi = r_w && sh.cum[r_w - 1] > gpos;
                         // fast path: the warp's whole slice lies in row r_w
-                        const uint64_t base = sh.rs[r_w];
+                        const uint32_t* __restrict__ cp = sh.rs[r_w] + a0 + lane;  // one address, then offsets
                         const uint64_t Trow = PM == kProbRow ? sh.thr[r_w] : g.gthr;
     #pragma unroll
                         for (int i = 0; i < U; ++i) {
-                            const uint32_t e = a0 + i * 32 + lane;
-                            const bool valid = e < total;
-                            v[i] = valid ? __ldg(g.col + base + e) : 0u;
-                            if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + base + e) : 0ull;
+                            const bool valid = a0 + i * 32 + lane < total;
+                            v[i] = valid ? __ldg(cp + i * 32) : 0u;
+                            if constexpr (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + (cp - g.col) + i * 32) : 0ull;
                             else T[i] = Trow;
                         }
                     } else {
@@ -770,9 +769,9 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rr
                             const uint32_t M = __reduce_or_sync(FULL, rel - 1 < 32 ? 1u << (rel - 1) : 0u);
                             const uint32_t rr = min(r + __popc(M & ((1u << lane) - 1u)), NB - 1);
                             r = min(r + __popc(M), NB - 1);
-                            const uint64_t eg = sh.rs[rr] + (uint64_t)ec;
-                            v[i] = valid ? __ldg(g.col + eg) : 0u;
-                            if (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + eg) : 0ull;
+                            const uint32_t* pp = sh.rs[rr] + ec;
+                            v[i] = valid ? __ldg(pp) : 0u;
+                            if constexpr (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + (pp - g.col)) : 0ull;
                             else if (PM == kProbRow) T[i] = sh.thr[rr];
                             else T[i] = g.gthr;
                         }
