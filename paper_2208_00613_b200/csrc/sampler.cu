@@ -1,22 +1,23 @@
 // sampler.cu -- RRR sampling on sm_100a (IC reverse BFS, LT reverse walk).
 //
 // Replaces the OpenMP loop of proj/src/sampler.cpp:85-104 (sample_block) and the body of
-// sample_rrr (sampler.cpp:14-45).  One warp owns one sample at a time (persistent grid,
-// dynamic work counter).  The sequential reference consumes one draw of the per-sample
-// stream (rng.hpp) per coin-tossing edge, in the order "adjacency rows of the members,
-// in member order".  The warp walks that flattened edge sequence in windows and assigns
-// draw numbers by ballot prefix:
-//   * an edge draws iff its target is unvisited *at that moment* and 0 < p < 1;
-//   * within one Gt row the targets are distinct (rows are deduplicated at upload, or the
-//     graph is flagged), so a group of U x 32 edges of one row is decided from the
-//     visited snapshot at the group start: U independent coins per lane (ILP);
-//   * a window that spans several rows may repeat a target: the window is committed up
-//     to the first lane whose target repeats an earlier candidate (match.any), and the
-//     rest is re-evaluated against the updated visited set.
-// Visited sets: a shared-memory bitmap over all n vertices when it fits, else a
-// shared-memory open-addressing hash with escalation (samples that overflow are
-// restarted from scratch -- the stream is a pure function of (seed, index) -- on a
-// bigger tier), and finally a per-warp global-memory bitmap.
+// sample_rrr (sampler.cpp:14-45).  The sequential reference consumes one draw of the
+// per-sample stream (rng.hpp) per coin-tossing edge, in the order "adjacency rows of the
+// members, in member order"; both kernels reproduce that stream exactly.
+//
+// IC (the hot path): rrr_block_kernel -- one CTA owns one sample (persistent grid, dynamic
+// work counter).  The flattened edge sequence of a batch of rows is consumed in groups of
+// NW*32*U edges decided from the visited snapshot at the group start, with CTA prefixes of
+// per-warp draw counts giving every lane its draw numbers; groups that span rows resolve
+// repeated targets exactly (see the block comment further down).  Visited set: a
+// shared-memory bitmap over all n when it fits (c1, c2); else a shared-memory hash whose
+// samples move in place to a promotion slot (a global bitmap + queue) at half its capacity;
+// without a free slot, or past the slot's queue, a sample restarts -- the stream is a pure
+// function of (seed, index) -- on a 128 KB hash tier and then a per-CTA global bitmap.
+//
+// LT (extension): rrr_kernel -- one warp owns one sample and walks single predecessors: a
+// 32-ary search over the row's cumulative in-weights picks the first edge whose running
+// sum exceeds the draw; the walk stops on a visited vertex, an empty row or r >= the sum.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -118,154 +119,6 @@ struct SampleResult {
     uint64_t probes = 0;  // LT: cumulative-weight entries read by the searches
 };
 
-template <int U, class Vis>
-__device__ __forceinline__ SampleResult bfs_ic(const GView& g, Vis& vis, uint32_t* __restrict__ q, uint32_t qcap,
-                               uint32_t root, uint64_t s0, uint64_t t) {
-    const uint32_t lane = lane_id();
-    const uint32_t lt = lanemask_lt();
-    uint32_t qhead = 0, qlen = 1;
-    uint64_t edges = 0;
-    if (lane == 0) {
-        q[0] = root;
-        vis.add(root);
-    }
-    __syncwarp();
-    while (qhead < qlen) {
-        // ---- batch of up to 32 rows (members qhead..qhead+nb) ----
-        const uint32_t nb = min(32u, qlen - qhead);
-        uint64_t rs = 0, thr_r = g.gthr;
-        uint32_t deg = 0;
-        if (lane < nb) {
-            const uint32_t u = q[qhead + lane];
-            rs = g.row[u];
-            deg = (uint32_t)(g.row[u + 1] - rs);
-            if (g.pmode == kProbRow) thr_r = g.thr[u];
-        }
-        uint32_t cum = deg;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(FULL, cum, o);
-            if (lane >= (uint32_t)o) cum += x;
-        }
-        const uint32_t total = __shfl_sync(FULL, cum, 31);
-        edges += total;
-        qhead += nb;
-        uint32_t pos = 0;
-        while (pos < total) {
-            // row holding flattened position pos (warp-uniform)
-            const uint32_t r = __popc(__ballot_sync(FULL, cum <= pos));
-            const uint32_t r_end = __shfl_sync(FULL, cum, r);
-            if (!g.row_dups && (r_end - pos >= 32 || r_end == total)) {
-                // ---------- single-row run: groups of U x 32 edges, no repeats ----------
-                const uint32_t r_deg = __shfl_sync(FULL, deg, r);
-                const uint64_t r_rs = __shfl_sync(FULL, rs, r);
-                const uint64_t r_thr = __shfl_sync(FULL, thr_r, r);
-                uint64_t e0 = r_rs + (pos - (r_end - r_deg));
-                uint32_t left = r_end - pos;
-                pos = r_end;
-                while (left > 0) {
-                    const uint32_t here = min(left, (uint32_t)(U * 32));
-                    uint32_t v[U];
-                    uint64_t tt[U];
-                    bool cand[U];
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        const uint32_t k = i * 32 + lane;
-                        v[i] = k < here ? __ldg(g.col + e0 + k) : 0u;
-                        tt[i] = r_thr;
-                        if (g.pmode == kProbEdge && k < here) tt[i] = __ldg(g.thr + e0 + k);
-                    }
-                    uint32_t dmask[U];
-                    uint32_t draws_before = 0;
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        const uint32_t k = i * 32 + lane;
-                        cand[i] = k < here && tt[i] != kThrNever && !vis.has(v[i]);
-                        dmask[i] = __ballot_sync(FULL, cand[i] && tt[i] != kThrAlways);
-                    }
-                    bool succ[U];
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        const uint64_t my_t = t + draws_before + __popc(dmask[i] & lt);
-                        succ[i] = cand[i] && (tt[i] == kThrAlways || coin_success(s0, my_t, tt[i]));
-                        draws_before += __popc(dmask[i]);
-                    }
-                    t += draws_before;
-#pragma unroll
-                    for (int i = 0; i < U; ++i) {
-                        const uint32_t sm = __ballot_sync(FULL, succ[i]);
-                        if (sm) {
-                            const uint32_t cnt = __popc(sm);
-                            if (qlen + cnt > qcap) return {qlen, edges, true};
-                            if (succ[i]) {
-                                q[qlen + __popc(sm & lt)] = v[i];
-                                vis.add(v[i]);
-                            }
-                            qlen += cnt;
-                        }
-                    }
-                    __syncwarp();
-                    e0 += here;
-                    left -= here;
-                }
-            } else {
-                // ---------- mixed window over several short rows ----------
-                const uint32_t gpos = pos + lane;
-                const bool valid = gpos < total;
-                // smallest row index rr with cum[rr] > gpos
-                uint32_t lo = 0, hi = 31;
-#pragma unroll
-                for (int s = 0; s < 5; ++s) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    const uint32_t c = __shfl_sync(FULL, cum, mid);
-                    if (c > gpos) hi = mid;
-                    else lo = mid + 1;
-                }
-                const uint32_t rr = valid ? lo : 31;
-                const uint32_t c_end = __shfl_sync(FULL, cum, rr);
-                const uint32_t c_deg = __shfl_sync(FULL, deg, rr);
-                const uint64_t c_rs = __shfl_sync(FULL, rs, rr);
-                uint64_t tsh = __shfl_sync(FULL, thr_r, rr);
-                uint32_t v = 0;
-                if (valid) {
-                    const uint64_t e = c_rs + (gpos - (c_end - c_deg));
-                    v = __ldg(g.col + e);
-                    if (g.pmode == kProbEdge) tsh = __ldg(g.thr + e);
-                }
-                const bool cand = valid && tsh != kThrNever && !vis.has(v);
-                // first lane whose candidate target repeats an earlier candidate
-                const unsigned long long key = cand ? (unsigned long long)v : (0x100000000ULL | lane);
-                const uint32_t peers = __match_any_sync(FULL, key);
-                const uint32_t dup = __ballot_sync(FULL, cand && (peers & lt) != 0);
-                const uint32_t cut = dup ? (uint32_t)(__ffs(dup) - 1) : 32u;
-                const bool in = lane < cut;
-                const uint32_t dm = __ballot_sync(FULL, in && cand && tsh != kThrAlways);
-                const uint64_t my_t = t + __popc(dm & lt);
-                const bool succ = in && cand && (tsh == kThrAlways || coin_success(s0, my_t, tsh));
-                t += __popc(dm);
-                const uint32_t sm = __ballot_sync(FULL, succ);
-                if (sm) {
-                    const uint32_t cnt = __popc(sm);
-                    if (qlen + cnt > qcap) return {qlen, edges, true};
-                    if (succ) {
-                        q[qlen + __popc(sm & lt)] = v;
-                        vis.add(v);
-                    }
-                    qlen += cnt;
-                }
-                __syncwarp();
-                pos += min(cut, total - pos);
-            }
-        }
-    }
-    return {qlen, edges, false};
-}
-
-// ------------------------------------------------------------------- LT walk ----
-// Extension (no reference implementation; oracle/immx_oracle.c oc_sample_lt is the
-// builder-defined contract): one draw r per step; the chosen in-edge is the first e of
-// the row with r < cum[e] (row-local running double sums, precomputed in CSR order);
-// stop on an empty row, r >= row sum, or an already visited target.
 template <class Vis>
 __device__ __forceinline__ SampleResult walk_lt(const GView& g, Vis& vis, uint32_t* __restrict__ q, uint32_t qcap,
                                 uint32_t root, uint64_t s0, uint64_t t) {
@@ -424,8 +277,8 @@ __global__ void __launch_bounds__(256) rrr_kernel(GView g, SampJob job, uint32_t
             root = (uint32_t)below(draw(s0, 1), g.n);
             t = 2;
         }
-        SampleResult res = job.model == IMMX_MODEL_LT ? walk_lt(g, vis, q, job.qcap, root, s0, t)
-                                                       : bfs_ic<U>(g, vis, q, job.qcap, root, s0, t);
+        // IC samples run in rrr_block_kernel; this warp-per-sample kernel serves the LT walks
+        SampleResult res = walk_lt(g, vis, q, job.qcap, root, s0, t);
         __syncwarp();
         if (!res.overflow) {
             // reserve exactly |R| arena slots and copy the set out
