@@ -883,7 +883,9 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         int mode = IMMX_MODE_RAW, char_mode = IMMX_MODE_RAW;
         double t_codebook = 0.0, t_lut = 0.0;  // host: Huffman tree, decode table
         double skew = 0.0, dens = 0.0;
-        HostCodebook cb;
+        if (!d.run_cb) d.run_cb = std::make_shared<HostCodebook>();
+        HostCodebook& cb = *d.run_cb;
+        cb.coded = 0;
         immx_store* store = nullptr;  // the device's run store (borrowed by the result)
         std::unique_ptr<immx_bitmap> bm;
         DBuf<unsigned int> hist;  // encoding-time table (huffman)
@@ -918,16 +920,19 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     std::vector<unsigned long long> leaves;
                     codebook_leaves_dev(d, h1.p, n, leaves);
                     const double t_leaves = secs(tc);
-                    cb = build_codebook_sorted(leaves.data(), leaves.size(), n);
+                    build_codebook_sorted(leaves.data(), leaves.size(), n, cb);
                     t_codebook = secs(tc);
                     if (std::getenv("IMMX_DEBUG_CODEBOOK"))
                         std::fprintf(stderr, "[immx codebook] coded %llu leaves (device sort + D2H) %.4f s, tree+codes %.4f s\n",
                                      (unsigned long long)leaves.size(), t_leaves, t_codebook - t_leaves);
                     const auto tl = Clock::now();
-                    std::vector<unsigned long long> lut;
+                    std::vector<unsigned long long>& lut = d.run_lut;
                     uint32_t rb = 1;
                     build_decode_lut(cb, lut, rb);
                     t_lut = secs(tl);
+                    if (std::getenv("IMMX_DEBUG_CODEBOOK"))
+                        std::fprintf(stderr, "[immx codebook] decode table %zu entries (root %u bits) %.4f s, nodes %zu\n",
+                                     lut.size(), rb, t_lut, cb.nodes.size());
                     if (!d.run_store) d.run_store = new immx_store;
                     store = d.run_store;
                     store->s.count = store->s.total_words = store->s.total_copied = store->s.payload_bytes = 0;

@@ -23,17 +23,19 @@ namespace {
 // once each equal-frequency run of merged nodes is ordered by min id at its first use.
 // Linear after the leaf sort, which the device does (codebook_leaves_dev).
 template <class F, class I>
-HostCodebook merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id, bool per_vertex) {
-    HostCodebook cb;
+void merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id, bool per_vertex, HostCodebook& cb) {
     if (per_vertex) {
         cb.bits.assign(n, 0);
         cb.len.assign(n, 0);
+    } else {
+        cb.bits.clear();
+        cb.len.clear();
     }
     cb.children_first = true;
     if (!L) fail(IMMX_ERUNTIME, "cannot build a codebook from an empty block");
     if (L >= (1ULL << 31)) fail(IMMX_EINVAL, "too many coded symbols");
     cb.coded = L;
-    cb.nodes.resize(L == 1 ? 2 : 2 * L - 1);
+    cb.nodes.assign(L == 1 ? 2 : 2 * L - 1, HostCodebook::Node{});
     for (uint64_t i = 0; i < L; ++i) cb.nodes[i].symbol = leaf_id(i);
     if (L == 1) {
         cb.nodes[1].child[0] = 0;
@@ -46,14 +48,15 @@ HostCodebook merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id, bool p
             cb.bits[leaf_id(0)] = 0;
             cb.len[leaf_id(0)] = 1;
         }
-        return cb;
+        return;
     }
     struct Q {
         uint64_t f;
         uint32_t minid;
         int32_t node;
     };
-    std::vector<Q> q;
+    static thread_local std::vector<Q> q;  // scratch, capacity kept across runs
+    q.clear();
     q.reserve(L - 1);
     uint64_t li = 0, qh = 0, ordered = 0;
     auto pop = [&](uint64_t& f, uint32_t& minid) -> int32_t {
@@ -90,8 +93,10 @@ HostCodebook merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id, bool p
     }
     cb.root = (int32_t)(2 * L - 2);
     // codes top-down: parents come after their children, so walk the merged nodes backwards
-    std::vector<uint64_t> pre(cb.nodes.size(), 0);
-    std::vector<uint8_t> dep(cb.nodes.size(), 0);
+    static thread_local std::vector<uint64_t> pre;
+    static thread_local std::vector<uint8_t> dep;
+    pre.assign(cb.nodes.size(), 0);
+    dep.assign(cb.nodes.size(), 0);
     for (int64_t u = cb.root; u >= (int64_t)L; --u) {
         if (dep[u] >= 64) fail(IMMX_ERUNTIME, "huffman code longer than 64 bits");
         for (int c = 0; c < 2; ++c) {
@@ -109,15 +114,15 @@ HostCodebook merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id, bool p
             cb.bits[cb.nodes[i].symbol] = pre[i];
             cb.len[cb.nodes[i].symbol] = dep[i];
         }
-    return cb;
 }
 
 }  // namespace
 
-HostCodebook build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n, bool per_vertex) {
-    return merge_sorted(
+void build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n, HostCodebook& cb,
+                           bool per_vertex) {
+    merge_sorted(
         count, n, [&](uint64_t i) { return (uint64_t)(leaves[i] >> 32); },
-        [&](uint64_t i) { return (uint32_t)(leaves[i] & 0xffffffffu); }, per_vertex);
+        [&](uint64_t i) { return (uint32_t)(leaves[i] & 0xffffffffu); }, per_vertex, cb);
 }
 
 HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n) {
@@ -125,8 +130,10 @@ HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n) {
     for (uint64_t v = 0; v < n; ++v)
         if (freq[v]) ids.push_back((uint32_t)v);
     std::stable_sort(ids.begin(), ids.end(), [&](uint32_t a, uint32_t b) { return freq[a] < freq[b]; });
-    return merge_sorted(
-        ids.size(), n, [&](uint64_t i) { return freq[ids[i]]; }, [&](uint64_t i) { return ids[i]; }, true);
+    HostCodebook cb;
+    merge_sorted(
+        ids.size(), n, [&](uint64_t i) { return freq[ids[i]]; }, [&](uint64_t i) { return ids[i]; }, true, cb);
+    return cb;
 }
 
 // Multi-level decode table (entry layout: huffman.cu header).  Table widths: root
@@ -134,7 +141,8 @@ HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n) {
 void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& lut, uint32_t& root_bits) {
     const size_t nn = cb.nodes.size();
     // subtree heights: children before parents in one index sweep
-    std::vector<uint32_t> height(nn, 0);
+    static thread_local std::vector<uint32_t> height;  // scratch, capacity kept across runs
+    height.assign(nn, 0);
     auto upd = [&](size_t u) {
         const auto& nd = cb.nodes[u];
         uint32_t h = 0;
@@ -146,7 +154,7 @@ void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& l
         for (size_t u = 0; u < nn; ++u) upd(u);
     else
         for (size_t u = nn; u-- > 0;) upd(u);
-    lut.clear();
+    lut.clear();  // keeps its capacity
     root_bits = std::max<uint32_t>(1, std::min<uint32_t>(12, height[cb.root]));
     struct Job {
         int32_t node;

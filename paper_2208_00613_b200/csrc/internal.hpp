@@ -123,6 +123,10 @@ struct Device {
     // the RRR pool of immx_run (reused by the next run on this device)
     struct ::immx_pool* run_pool = nullptr;
     struct ::immx_store* run_store = nullptr;  // likewise the run's Huffman store
+    // host-side buffers of the run's Huffman tree and decode table, reused so repeated runs
+    // do not pay first-touch page faults on ~100 MB of fresh host memory
+    std::shared_ptr<struct HostCodebook> run_cb;
+    std::vector<unsigned long long> run_lut;
 };
 
 struct DevGraph {
@@ -338,8 +342,9 @@ struct HostCodebook {
 };
 HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n);
 // leaves = the coded vertices as (freq << 32 | id), sorted ascending
-HostCodebook build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n,
-                                   bool per_vertex = false);
+// fills `cb` in place (its vectors' capacity is reused)
+void build_codebook_sorted(const unsigned long long* leaves, uint64_t count, uint64_t n, HostCodebook& cb,
+                           bool per_vertex = false);
 void codebook_leaves_dev(Device& d, const unsigned int* d_hist, uint64_t n, std::vector<unsigned long long>& leaves);
 void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& lut, uint32_t& root_bits);
 
