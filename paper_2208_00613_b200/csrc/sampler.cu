@@ -29,6 +29,10 @@
 
 #include "internal.hpp"
 
+#ifndef IMMX_MINB
+#define IMMX_MINB 4  // resident 8-warp CTAs per SM the register budget is set for
+#endif
+
 namespace immx_dev {
 
 constexpr uint32_t FULL = 0xffffffffu;
@@ -451,7 +455,7 @@ __device__ __forceinline__ void warp_prefix(const uint32_t* a, uint32_t w, uint3
 }
 
 template <int KIND, int PM, int NW, int U>
-__global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : 4)) rrr_block_kernel(GView g, SampJob job, uint32_t vis_words) {
+__global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : IMMX_MINB)) rrr_block_kernel(GView g, SampJob job, uint32_t vis_words) {
     extern __shared__ uint32_t dsm[];
     __shared__ BlkSmem<NW, U> sh;
     constexpr uint32_t NB = NW * 32;
