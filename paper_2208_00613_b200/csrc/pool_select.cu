@@ -1,12 +1,8 @@
-// pool_select.cu -- histograms, argmax and greedy max-coverage over the raw pool.
-//
-// table_argmax (select.cpp:10-20): max over the packed key (count << 32 | ~id), so the
-// largest count wins and ties go to the lowest id; an all-zero table gives id 0.
-// select_raw (select.cpp:89-148) recounts the frequency table over the live sets every
-// round.  The device keeps one table and an inverted index (vertex -> sets holding it)
-// instead: covering pick's sets subtracts exactly their members from the table, which
-// leaves the same counts the recount would produce, so seeds, marginals and coverage are
-// identical while each round touches only the newly covered sets.
+// pool_select.cu -- the raw pool on the device: vertex histograms (update_hist,
+// pipeline.cpp:26-43), table_argmax (select.cpp:10-20: max over the packed key
+// count << 32 | ~id, so the largest count wins and ties go to the lowest id; an all-zero
+// table gives id 0), the Huffman leaf list, pool upload/download and small conversions.
+// (select_raw itself is in select.cu.)
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -81,63 +77,6 @@ __global__ void k_argmax(const unsigned int* __restrict__ hist, uint64_t n, unsi
             best = x > best ? x : best;
         }
         if (threadIdx.x == 0 && best) atomicMax(out, best);
-    }
-}
-
-// fill the inverted index: idx[cursor[v]++] = set id
-__global__ void k_index_fill(const uint32_t* __restrict__ arena, const uint64_t* __restrict__ off,
-                             const uint32_t* __restrict__ len, uint64_t count, unsigned long long* __restrict__ cursor,
-                             uint32_t* __restrict__ idx) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t j = w; j < count; j += nw) {
-        const uint64_t b = off[j];
-        const uint32_t l = len[j];
-        for (uint32_t i = lane; i < l; i += 32) idx[atomicAdd(&cursor[arena[b + i]], 1ULL)] = (uint32_t)j;
-    }
-}
-
-// one thread: decode the argmax key of round r, pad when the gain is 0 (select.cpp:47-57)
-__global__ void k_round_pick(unsigned long long* __restrict__ keys, uint32_t r, uint8_t* __restrict__ is_seed,
-                             uint32_t* __restrict__ seeds, unsigned long long* __restrict__ marg,
-                             uint32_t* __restrict__ cover_pick, uint64_t n) {
-    const unsigned long long key = keys[r];
-    uint32_t pick = 0xffffffffu - (uint32_t)(key & 0xffffffffu);
-    const uint32_t gain = (uint32_t)(key >> 32);
-    if (key == 0) pick = 0;  // all-zero table: table_argmax returns 0
-    if (gain == 0) {
-        uint32_t p = 0;
-        while (p < n && is_seed[p]) ++p;
-        pick = p;
-        *cover_pick = 0xffffffffu;
-    } else {
-        *cover_pick = pick;
-    }
-    is_seed[pick] = 1;
-    seeds[r] = pick;
-    marg[r] = gain;
-}
-
-// warp per set of bucket(pick): mark covered, subtract its members from the table
-__global__ void k_cover_raw(const uint32_t* __restrict__ arena, const uint64_t* __restrict__ off,
-                            const uint32_t* __restrict__ len, const uint64_t* __restrict__ idx_off,
-                            const uint32_t* __restrict__ idx, const uint32_t* __restrict__ cover_pick,
-                            uint8_t* __restrict__ covered, unsigned int* __restrict__ hist) {
-    const uint32_t pick = *cover_pick;
-    if (pick == 0xffffffffu) return;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t b0 = idx_off[pick], b1 = idx_off[pick + 1];
-    for (uint64_t q = b0 + w; q < b1; q += nw) {
-        const uint32_t s = idx[q];
-        if (covered[s]) continue;
-        __syncwarp();
-        if (lane == 0) covered[s] = 1;
-        const uint64_t b = off[s];
-        const uint32_t l = len[s];
-        for (uint32_t i = lane; i < l; i += 32) atomicSub(&hist[arena[b + i]], 1u);
     }
 }
 
