@@ -388,7 +388,7 @@ struct BHash {  // CTA-shared linear-probing hash, load <= 1/2
     __device__ void clear_members(const uint32_t*, uint32_t) { clear_all(); }
 };
 
-enum BVisKind { kBBits = 0, kBHash13 = 1, kBHash15 = 2, kBGlob = 3 };
+enum BVisKind { kBBits = 0, kBHash13 = 1, kBHash15 = 2, kBGlob = 3, kBBitsS = 4 };
 template <int K>
 struct BVisOf;
 template <>
@@ -399,6 +399,8 @@ template <>
 struct BVisOf<kBHash15> { using T = BHash<15>; };
 template <>
 struct BVisOf<kBGlob> { using T = BGBits; };
+template <>
+struct BVisOf<kBBitsS> { using T = BBits; };  // the same bitmap, 4-warp CTAs (small graphs)
 
 template <int NW, int U>
 struct BlkSmem {
@@ -455,7 +457,7 @@ __device__ __forceinline__ void warp_prefix(const uint32_t* a, uint32_t w, uint3
 }
 
 template <int KIND, int PM, int NW, int U>
-__global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : IMMX_MINB)) rrr_block_kernel(GView g, SampJob job, uint32_t vis_words) {
+__global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >= 8 ? IMMX_MINB : 8))) rrr_block_kernel(GView g, SampJob job, uint32_t vis_words) {
     extern __shared__ uint32_t dsm[];
     __shared__ BlkSmem<NW, U> sh;
     constexpr uint32_t NB = NW * 32;
@@ -468,7 +470,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : IMMX_M
     uint32_t qcap = job.qcap;
     uint32_t* pw = nullptr;  // promoted: the slot's global visited bitmap (CTA-uniform)
     typename BVisOf<KIND>::T vis;
-    if constexpr (KIND == kBBits) {
+    if constexpr ((KIND == kBBits || KIND == kBBitsS)) {
         vis.w = dsm;
         vis.words = vis_words;
     } else if constexpr (KIND == kBGlob) {
@@ -663,7 +665,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : IMMX_M
                     // for a whole group.  Otherwise check the capacity first (stotal may count a
                     // repeated target twice -- then the sample just moves to the next tier).
                     const bool early = P ? qlen + G <= qcap
-                                         : (KIND == kBBits || KIND == kBGlob || qlen + sh.hdup + G <= qcap);
+                                         : ((KIND == kBBits || KIND == kBBitsS) || KIND == kBGlob || qlen + sh.hdup + G <= qcap);
                     bool flag = false;
                     if (early) {
     #pragma unroll
@@ -766,9 +768,9 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : IMMX_M
                         qlen += s2t;
                         t += d2t;
                         if (cut != 0xffffffffu) {
-                            bool bitmap_vis = KIND == kBBits || KIND == kBGlob;
+                            bool bitmap_vis = (KIND == kBBits || KIND == kBBitsS) || KIND == kBGlob;
                             uint32_t* bw = nullptr;
-                            if constexpr (KIND == kBBits || KIND == kBGlob) bw = vis.w;
+                            if constexpr ((KIND == kBBits || KIND == kBBitsS) || KIND == kBGlob) bw = vis.w;
                             if constexpr (P) {
                                 bitmap_vis = true;
                                 bw = pw;
@@ -929,7 +931,7 @@ constexpr int kBlkU = IMMX_BLK_U;
 #endif
 template <int KIND>
 struct BlkShape {
-    static constexpr int NW = (KIND == kBHash15 || KIND == kBGlob) ? IMMX_BIG_NW : kBlkNW;
+    static constexpr int NW = (KIND == kBHash15 || KIND == kBGlob) ? IMMX_BIG_NW : (KIND == kBBitsS ? 4 : kBlkNW);
     static constexpr int U = (KIND == kBHash15 || KIND == kBGlob) ? IMMX_BIG_U : kBlkU;
 };
 
@@ -1060,7 +1062,11 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     if (model == IMMX_MODEL_IC) {
         // CTA-cooperative tiers: a CTA-shared bitmap when n/8 <= 64 KB, else CTA-shared hashes
         // escalating to a per-CTA global bitmap
-        if (nwords * 4 <= 64 * 1024) {
+        if (nwords * 4 <= 8 * 1024) {
+            // small graphs (config 1): short BFS levels make a sample latency-bound, so run
+            // twice as many CTAs of half the width
+            tiers.push_back({kBBitsS, (uint32_t)nwords, 4, ncap, true, 0});
+        } else if (nwords * 4 <= 64 * 1024) {
             tiers.push_back({kBBits, (uint32_t)nwords, kBlkNW, ncap, true, 0});
         } else {
             tiers.push_back({kBHash13, 1u << 13, kBlkNW, 1u << 12, true, 0});
@@ -1136,6 +1142,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
             const size_t smem = (size_t)tier.smem_words_per_warp * 4;
             switch (tier.kind) {
                 case kBBits: warps = block_grid<kBBits>(d, tier, smem); break;
+                case kBBitsS: warps = block_grid<kBBitsS>(d, tier, smem); break;
                 case kBHash13: warps = block_grid<kBHash13>(d, tier, smem); break;
                 case kBHash15: warps = block_grid<kBHash15>(d, tier, smem); break;
                 default: warps = block_grid<kBGlob>(d, tier, smem); break;
@@ -1163,6 +1170,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         if (tier.block) {
             switch (tier.kind) {
                 case kBBits: launch_block_tier<kBBits>(d, gv, job, tier, nitems, warps); break;
+                case kBBitsS: launch_block_tier<kBBitsS>(d, gv, job, tier, nitems, warps); break;
                 case kBHash13: launch_block_tier<kBHash13>(d, gv, job, tier, nitems, warps); break;
                 case kBHash15: launch_block_tier<kBHash15>(d, gv, job, tier, nitems, warps); break;
                 default: launch_block_tier<kBGlob>(d, gv, job, tier, nitems, warps); break;
