@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libimmx_b200.so")
+# IMMX_B200_LIB: an alternative in-tree build of the same library (kernel experiments)
+LIB_PATH = os.environ.get("IMMX_B200_LIB") or os.path.join(HERE, "libimmx_b200.so")
 
 OK, EINVAL, ERUNTIME, ERANGE, ECUDA = 0, 1, 2, 3, 4
 MODE_HUFFMAN, MODE_BITMAP, MODE_RAW, MODE_HYBRID, MODE_AUTO = 0, 1, 2, 3, -1

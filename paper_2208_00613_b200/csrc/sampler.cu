@@ -30,7 +30,10 @@
 #include "internal.hpp"
 
 #ifndef IMMX_MINB
-#define IMMX_MINB 4  // resident 8-warp CTAs per SM the register budget is set for
+#define IMMX_MINB 5  // resident 8-warp CTAs per SM the register budget is set for (global / per-edge p)
+#endif
+#ifndef IMMX_MINB_ROW
+#define IMMX_MINB_ROW 4  // the same with per-row p (its row-threshold array leaves room for 4)
 #endif
 
 namespace immx_dev {
@@ -402,11 +405,11 @@ struct BVisOf<kBGlob> { using T = BGBits; };
 template <>
 struct BVisOf<kBBitsS> { using T = BBits; };  // the same bitmap, 4-warp CTAs (small graphs)
 
-template <int NW, int U>
+template <int NW, int U, int PM>
 struct BlkSmem {
     const uint32_t* rs[NW * 32];  // &col[flattened position 0 of the row] (row start - exclusive cum)
     uint32_t cum[NW * 32];   // inclusive prefix of the batch's row degrees
-    uint64_t thr[NW * 32];   // row threshold (global / per-row modes)
+    uint64_t thr[PM == kProbRow ? NW * 32 : 1];  // row thresholds (per-row mode only)
     alignas(16) uint32_t wsum[NW];
     alignas(16) uint32_t wsum2[NW];
     uint32_t nextrow[2][NW];  // rows of the next group's warp starts (double-buffered)
@@ -457,9 +460,9 @@ __device__ __forceinline__ void warp_prefix(const uint32_t* a, uint32_t w, uint3
 }
 
 template <int KIND, int PM, int NW, int U>
-__global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >= 8 ? IMMX_MINB : 8))) rrr_block_kernel(GView g, SampJob job, uint32_t vis_words) {
+__global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >= 8 ? (PM == kProbRow ? IMMX_MINB_ROW : IMMX_MINB) : 8))) rrr_block_kernel(GView g, SampJob job, uint32_t vis_words) {
     extern __shared__ uint32_t dsm[];
-    __shared__ BlkSmem<NW, U> sh;
+    __shared__ BlkSmem<NW, U, PM> sh;
     constexpr uint32_t NB = NW * 32;
     constexpr uint32_t G = NW * 32 * U;
     const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -667,7 +670,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     const bool early = P ? qlen + G <= qcap
                                          : ((KIND == kBBits || KIND == kBBitsS) || KIND == kBGlob || qlen + sh.hdup + G <= qcap);
                     bool flag = false;
-                    if (early) {
+                    if (early && ws) {  // (ws: warp-uniform; most warps of a group have no success)
     #pragma unroll
                         for (int i = 0; i < U; ++i)
                             if (succ[i]) flag |= vadd(v[i]);
@@ -695,11 +698,13 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     }
                     if (!conflict) {
                         // common case: commit the whole group
-                        uint32_t p = qlen + sbefore;
+                        if (ws) {
+                            uint32_t p = qlen + sbefore;
     #pragma unroll
-                        for (int i = 0; i < U; ++i) {
-                            if (succ[i]) q[p + __popc(sm[i] & lt)] = v[i];
-                            p += __popc(sm[i]);
+                            for (int i = 0; i < U; ++i) {
+                                if (succ[i]) q[p + __popc(sm[i] & lt)] = v[i];
+                                p += __popc(sm[i]);
+                            }
                         }
                         qlen += stotal;
                         t += dtotal;
@@ -936,7 +941,7 @@ struct BlkShape {
 };
 
 template <int KIND>
-uint32_t block_grid(Device& d, const Tier& tier, size_t smem) {
+uint32_t block_grid(Device& d, const Tier& tier, size_t smem, int pmode) {
     constexpr int NW = BlkShape<KIND>::NW, U = BlkShape<KIND>::U;
     for (auto kern : {rrr_block_kernel<KIND, kProbGlobal, NW, U>, rrr_block_kernel<KIND, kProbRow, NW, U>,
                       rrr_block_kernel<KIND, kProbEdge, NW, U>}) {
@@ -944,7 +949,10 @@ uint32_t block_grid(Device& d, const Tier& tier, size_t smem) {
         if (smem) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
-    auto kern = rrr_block_kernel<KIND, kProbEdge, NW, U>;
+    // occupancy of the variant that runs (register budget and static shared memory differ)
+    auto kern = pmode == kProbGlobal ? rrr_block_kernel<KIND, kProbGlobal, NW, U>
+              : pmode == kProbRow    ? rrr_block_kernel<KIND, kProbRow, NW, U>
+                                     : rrr_block_kernel<KIND, kProbEdge, NW, U>;
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem));
     if (per_sm < 1) fail(IMMX_ECUDA, "sampler tier does not fit on an SM");
@@ -1141,11 +1149,11 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         if (tier.block) {
             const size_t smem = (size_t)tier.smem_words_per_warp * 4;
             switch (tier.kind) {
-                case kBBits: warps = block_grid<kBBits>(d, tier, smem); break;
-                case kBBitsS: warps = block_grid<kBBitsS>(d, tier, smem); break;
-                case kBHash13: warps = block_grid<kBHash13>(d, tier, smem); break;
-                case kBHash15: warps = block_grid<kBHash15>(d, tier, smem); break;
-                default: warps = block_grid<kBGlob>(d, tier, smem); break;
+                case kBBits: warps = block_grid<kBBits>(d, tier, smem, gv.pmode); break;
+                case kBBitsS: warps = block_grid<kBBitsS>(d, tier, smem, gv.pmode); break;
+                case kBHash13: warps = block_grid<kBHash13>(d, tier, smem, gv.pmode); break;
+                case kBHash15: warps = block_grid<kBHash15>(d, tier, smem, gv.pmode); break;
+                default: warps = block_grid<kBGlob>(d, tier, smem, gv.pmode); break;
             }
         } else {
             warps = grid_warps(d, tier);
@@ -1193,8 +1201,8 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         members += hctl->members;
         const uint32_t n_ovf = hctl->n_ovf, n_nospace = hctl->n_nospace;
         if (debug_tiers())
-            std::fprintf(stderr, "[immx sampler] tier %d%s items %u ovf %u nospace %u members %llu edges %llu abandoned %llu promoted %llu %.3f ms\n",
-                         tier.kind, tier.block ? "b" : "w", nitems, n_ovf, n_nospace,
+            std::fprintf(stderr, "[immx sampler] tier %d%s grid %u items %u ovf %u nospace %u members %llu edges %llu abandoned %llu promoted %llu %.3f ms\n",
+                         tier.kind, tier.block ? "b" : "w", warps, nitems, n_ovf, n_nospace,
                          (unsigned long long)hctl->members, (unsigned long long)hctl->edges,
                          (unsigned long long)hctl->edges_abandoned, (unsigned long long)hctl->n_promoted,
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_launch).count());
