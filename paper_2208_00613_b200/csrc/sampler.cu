@@ -357,11 +357,23 @@ struct BGBits : BBits {  // global-memory bitmap: loads bypass L1 (atomics live 
 };
 
 template <int LOGH>
-struct BHash {  // CTA-shared linear-probing hash, load <= 1/2
-    uint32_t* s;
+struct BHash {  // CTA-shared linear-probing hash (load <= 1/2) behind a one-hash bit filter
+    // Most probes are of unvisited targets (c4: 99%), so the filter -- 2^(LOGH+3) bits, a bit per
+    // key hashed independently of the slot -- answers them with one branch-free word test; only
+    // members and filter collisions (|R| / 2^(LOGH+3)) walk the probe chain.  Bits are never
+    // cleared mid-sample (a rolled-back key just leaves a false positive).
+    uint32_t* s;  // H slots
+    uint32_t* f;  // FW filter words (right after the slots)
     static constexpr uint32_t H = 1u << LOGH;
+    static constexpr uint32_t LOGF = LOGH + 3;
+    static constexpr uint32_t FW = (1u << LOGF) / 32;
     __device__ static uint32_t h(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - LOGH); }
-    __device__ bool has(uint32_t v) const {
+    __device__ static uint32_t fh(uint32_t v) { return (v * 0x85EBCA6Bu) >> (32 - LOGF); }
+    __device__ bool maybe(uint32_t v) const {
+        const uint32_t b = fh(v);
+        return (f[b >> 5] >> (b & 31)) & 1u;
+    }
+    __device__ bool probe(uint32_t v) const {
         uint32_t i = h(v);
         for (;;) {
             const uint32_t k = s[i];
@@ -370,7 +382,10 @@ struct BHash {  // CTA-shared linear-probing hash, load <= 1/2
             i = (i + 1) & (H - 1);
         }
     }
+    __device__ bool has(uint32_t v) const { return maybe(v) && probe(v); }
     __device__ bool add_test(uint32_t v) {
+        const uint32_t b = fh(v);
+        atomicOr(&f[b >> 5], 1u << (b & 31));
         uint32_t i = h(v);
         for (;;) {
             const uint32_t old = atomicCAS(&s[i], kEmptyKey, v);
@@ -387,6 +402,7 @@ struct BHash {  // CTA-shared linear-probing hash, load <= 1/2
     __device__ void clear_all() {
         const uint4 e = make_uint4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
         for (uint32_t i = threadIdx.x; i < H / 4; i += blockDim.x) reinterpret_cast<uint4*>(s)[i] = e;
+        for (uint32_t i = threadIdx.x; i < FW / 4; i += blockDim.x) reinterpret_cast<uint4*>(f)[i] = make_uint4(0, 0, 0, 0);
     }
     __device__ void clear_members(const uint32_t*, uint32_t) { clear_all(); }
 };
@@ -415,8 +431,7 @@ struct BlkSmem {
     uint32_t nextrow[2][NW];  // rows of the next group's warp starts (double-buffered)
     uint32_t hdup;            // hash tiers: duplicate keys left by conflict rollbacks
     int pslot;                // hash tiers: the promotion slot taken (-1: none)
-    uint32_t lpos[NW * 32 * U];  // rare path: success positions
-    uint32_t lv[NW * 32 * U];    //            and targets
+    uint32_t lbuf[2 * NW * 32 * U];  // rare path: success positions (lbuf[0, G)) and targets (lbuf[G, 2G))
     uint32_t cut;
     uint32_t j;
     unsigned long long base;
@@ -481,6 +496,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
         vis.words = vis_words;
     } else {
         vis.s = dsm;
+        vis.f = dsm + BVisOf<KIND>::T::H;
     }
     if constexpr (KIND != kBGlob) vis.clear_all();  // the host zeroes global bitmaps
     __syncthreads();
@@ -719,8 +735,8 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                             for (int i = 0; i < U; ++i) {
                                 if (succ[i]) {
                                     const uint32_t k = p + __popc(sm[i] & lt);
-                                    sh.lpos[k] = gpos + (w * U + i) * 32 + lane;
-                                    sh.lv[k] = v[i];
+                                    sh.lbuf[k] = gpos + (w * U + i) * 32 + lane;
+                                    sh.lbuf[G + k] = v[i];
                                 }
                                 p += __popc(sm[i]);
                             }
@@ -733,7 +749,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                             const uint32_t pos = gpos + (w * U + i) * 32 + lane;
                             uint32_t minp = 0xffffffffu;
                             for (uint32_t k = 0; k < stotal; ++k)
-                                if (sh.lv[k] == v[i]) minp = min(minp, sh.lpos[k]);
+                                if (sh.lbuf[G + k] == v[i]) minp = min(minp, sh.lbuf[k]);
                             if (minp < pos) atomicMin(&sh.cut, pos);
                         }
                         __syncthreads();
@@ -1077,8 +1093,9 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         } else if (nwords * 4 <= 64 * 1024) {
             tiers.push_back({kBBits, (uint32_t)nwords, kBlkNW, ncap, true, 0});
         } else {
-            tiers.push_back({kBHash13, 1u << 13, kBlkNW, 1u << 12, true, 0});
-            tiers.push_back({kBHash15, 1u << 15, kBlkNW, 1u << 14, true, 0});
+            // (shared words: the hash slots + its filter, 2^(LOGH+3) bits)
+            tiers.push_back({kBHash13, (1u << 13) + (1u << 11), kBlkNW, 1u << 12, true, 0});
+            tiers.push_back({kBHash15, (1u << 15) + (1u << 13), kBlkNW, 1u << 14, true, 0});
             tiers.push_back({kBGlob, 0, kBlkNW, ncap, true, 64});
         }
     } else if (nwords * 4 <= 40 * 1024) {
