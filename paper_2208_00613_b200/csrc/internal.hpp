@@ -137,6 +137,7 @@ struct DevGraph {
     int pmode = kProbGlobal;
     uint64_t gthr = 0;      // global threshold
     DBuf<uint64_t> thr;     // per-row or per-edge thresholds
+    mutable DBuf<uint64_t> thr_fill;  // global p of 0 or 1: the same value per row (sampler)
     DBuf<double> lt_cum;    // LT: per-edge running weight sums in CSR order (row-local)
     bool has_lt = false;
     bool row_dups = false;  // some Gt row holds a repeated target

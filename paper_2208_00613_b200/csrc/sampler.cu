@@ -72,6 +72,17 @@ __device__ __forceinline__ bool coin_success(uint64_t s0, uint64_t t, uint64_t t
     return xlo < (uint32_t)tsh;
 }
 
+// High word of the draw (the success test on it alone is exact unless it equals the
+// threshold's high word: callers resolve those rare ties with coin_success).
+__device__ __forceinline__ uint32_t coin_xhi(uint64_t s0, uint64_t t) {
+    uint64_t z = s0 + t * kGamma;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    const uint64_t y = z ^ (z >> 27);
+    const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
+    const uint32_t zhi = __umulhi(ylo, 0x133111ebu) + ylo * 0x94d049bbu + yhi * 0x133111ebu;
+    return zhi ^ (zhi >> 31);
+}
+
 // ---------------------------------------------------------------- visited sets ----
 struct SmemBits {  // n bits in shared memory; never overflows
     uint32_t* w;
@@ -657,8 +668,9 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
     #pragma unroll
                     for (int i = 0; i < U; ++i) {
                         const bool valid = a0 + i * 32 + lane < total;
-                        cand[i] = valid && T[i] != kThrNever && !vhas(v[i]);
-                        dm[i] = __ballot_sync(FULL, cand[i] && T[i] != kThrAlways);
+                        // (global p is never 0 or 1 here: those graphs run as per-row thresholds)
+                        cand[i] = valid && (PM == kProbGlobal || T[i] != kThrNever) && !vhas(v[i]);
+                        dm[i] = __ballot_sync(FULL, cand[i] && (PM == kProbGlobal || T[i] != kThrAlways));
                         wd += __popc(dm[i]);
                     }
                     if (lane == 0) sh.wsum[w] = wd;
@@ -670,11 +682,27 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     uint32_t sm[U];
                     uint32_t ws = 0;
                     uint64_t tb = t + dbefore;
+                    bool coin[U];
+                    uint32_t tie = 0;
+    #pragma unroll
+                    for (int i = 0; i < U; ++i) {  // branch-free, on the draws' high words
+                        const uint32_t xh = coin_xhi(s0, tb + __popc(dm[i] & lt));
+                        const uint32_t th = (uint32_t)(T[i] >> 32);
+                        coin[i] = xh < th;
+                        tie |= (uint32_t)(xh == th) << i;
+                        tb += __popc(dm[i]);
+                    }
+                    if (__any_sync(FULL, tie)) {  // rare (2^-32 a draw): equal high words, the low words decide
+                        uint64_t tb2 = t + dbefore;
+    #pragma unroll
+                        for (int i = 0; i < U; ++i) {
+                            if ((tie >> i) & 1u) coin[i] = coin_success(s0, tb2 + __popc(dm[i] & lt), T[i]);
+                            tb2 += __popc(dm[i]);
+                        }
+                    }
     #pragma unroll
                     for (int i = 0; i < U; ++i) {
-                        const bool coin = coin_success(s0, tb + __popc(dm[i] & lt), T[i]);  // branch-free
-                        succ[i] = cand[i] && (T[i] == kThrAlways || coin);
-                        tb += __popc(dm[i]);
+                        succ[i] = cand[i] && ((PM != kProbGlobal && T[i] == kThrAlways) || coin[i]);
                         sm[i] = __ballot_sync(FULL, succ[i]);
                         ws += __popc(sm[i]);
                     }
@@ -974,6 +1002,8 @@ uint32_t block_grid(Device& d, const Tier& tier, size_t smem, int pmode) {
     if (per_sm < 1) fail(IMMX_ECUDA, "sampler tier does not fit on an SM");
     uint32_t blocks = (uint32_t)per_sm * (uint32_t)d.num_sms;
     if (tier.max_blocks) blocks = std::min(blocks, tier.max_blocks);
+    if (const char* e = std::getenv("IMMX_SAMPLER_CTAS"))  // measurement knob: cap the sampler grid
+        if (std::atoi(e) > 0) blocks = std::min<uint32_t>(blocks, (uint32_t)std::atoi(e));
     return blocks;
 }
 
@@ -1124,6 +1154,14 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     nospace.exact(count);
 
     GView gv = make_view(G);
+    if (G.pmode == kProbGlobal && (G.gthr == kThrNever || G.gthr == kThrAlways)) {
+        // p = 0 or p >= 1 everywhere: no coin is ever tossed; run as per-row thresholds (one
+        // filled array) so the global-p kernels need no special cases
+        G.thr_fill.exact(G.n);
+        CK(cudaMemsetAsync(G.thr_fill.p, G.gthr == kThrNever ? 0x00 : 0xff, G.n * 8, s));
+        gv.thr = G.thr_fill.p;
+        gv.pmode = kProbRow;
+    }
     SampJob job{};
     if (model == IMMX_MODEL_IC && nwords * 4 > 64 * 1024) {
         // promotion slots for the hash tier: one per resident CTA where ~4 GB allow, each a
