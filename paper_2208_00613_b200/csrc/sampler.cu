@@ -494,6 +494,9 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
     const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t lt = lanemask_lt();
     constexpr bool kHash = KIND == kBHash13 || KIND == kBHash15;
+    // invalid positions (past the batch) load the root instead of being tested: fewer integer
+    // instructions, but one more live register -- a loss at the global-p kernels' 48 registers
+    constexpr bool kRootFill = PM != kProbGlobal;
     uint32_t* const qbase = job.qscratch + (size_t)blockIdx.x * job.qcap;
     uint32_t* q = qbase;
     uint32_t qcap = job.qcap;
@@ -626,6 +629,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                         const uint32_t x = gpos + G + lane * U * 32;
                         if (lane < (uint32_t)NW && x < total) sh.nextrow[par ^ 1][lane] = advance_row<NW>(sh.cum, r_w, x);
                     }
+                    const int lim = (int)(total - a0) - (int)lane;  // position a0 + i*32 + lane is valid iff i*32 < lim
                     // this warp's slice leaves the row holding gpos -> the group spans several rows
                     bool my_multi = false;
                     if (a0 < total && sh.cum[r_w] >= min(a0 + U * 32, total)) {
@@ -635,8 +639,8 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                         const uint64_t Trow = PM == kProbRow ? sh.thr[r_w] : g.gthr;
     #pragma unroll
                         for (int i = 0; i < U; ++i) {
-                            const bool valid = a0 + i * 32 + lane < total;
-                            v[i] = valid ? __ldg(cp + i * 32) : 0u;
+                            const bool valid = kRootFill ? (int)i * 32 < lim : a0 + i * 32 + lane < total;
+                            v[i] = valid ? __ldg(cp + i * 32) : (kRootFill ? root : 0u);
                             if constexpr (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + (cp - g.col) + i * 32) : 0ull;
                             else T[i] = Trow;
                         }
@@ -659,7 +663,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                             const uint32_t rr = min(r + __popc(M & ((1u << lane) - 1u)), NB - 1);
                             r = min(r + __popc(M), NB - 1);
                             const uint32_t* pp = sh.rs[rr] + ec;
-                            v[i] = valid ? __ldg(pp) : 0u;
+                            v[i] = valid ? __ldg(pp) : (kRootFill ? root : 0u);
                             if constexpr (PM == kProbEdge) T[i] = valid ? __ldg(g.thr + (pp - g.col)) : 0ull;
                             else if (PM == kProbRow) T[i] = sh.thr[rr];
                             else T[i] = g.gthr;
@@ -667,19 +671,27 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     }
     #pragma unroll
                     for (int i = 0; i < U; ++i) {
-                        const bool valid = a0 + i * 32 + lane < total;
-                        // (global p is never 0 or 1 here: those graphs run as per-row thresholds)
+                        // kRootFill: positions past the batch hold the root, which is always
+                        // visited.  (Global p is never 0 or 1 here: those graphs run as per-row
+                        // thresholds.)
+                        const bool valid = kRootFill || a0 + i * 32 + lane < total;
                         cand[i] = valid && (PM == kProbGlobal || T[i] != kThrNever) && !vhas(v[i]);
                         dm[i] = __ballot_sync(FULL, cand[i] && (PM == kProbGlobal || T[i] != kThrAlways));
                         wd += __popc(dm[i]);
                     }
+                    // per-lane flags re-derived from the warp masks (no bool arrays to keep live):
+                    // with global p a candidate is exactly a drawing lane
+                    auto CAND = [&](int i) -> bool {
+                        if constexpr (PM == kProbGlobal) return (dm[i] >> lane) & 1u;
+                        else return cand[i];
+                    };
                     if (lane == 0) sh.wsum[w] = wd;
                     // barrier + "does the group span several rows" in one instruction
                     const bool multi = __syncthreads_or(my_multi) || g.row_dups;
                     uint32_t dbefore, dtotal;
                     warp_prefix<NW>(sh.wsum, w, dbefore, dtotal);
-                    bool succ[U];
                     uint32_t sm[U];
+                    auto SUCC = [&](int i) -> bool { return (sm[i] >> lane) & 1u; };
                     uint32_t ws = 0;
                     uint64_t tb = t + dbefore;
                     bool coin[U];
@@ -702,8 +714,8 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     }
     #pragma unroll
                     for (int i = 0; i < U; ++i) {
-                        succ[i] = cand[i] && ((PM != kProbGlobal && T[i] == kThrAlways) || coin[i]);
-                        sm[i] = __ballot_sync(FULL, succ[i]);
+                        const bool succ = CAND(i) && ((PM != kProbGlobal && T[i] == kThrAlways) || coin[i]);
+                        sm[i] = __ballot_sync(FULL, succ);
                         ws += __popc(sm[i]);
                     }
                     if (lane == 0) sh.wsum2[w] = ws;
@@ -717,7 +729,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     if (early && ws) {  // (ws: warp-uniform; most warps of a group have no success)
     #pragma unroll
                         for (int i = 0; i < U; ++i)
-                            if (succ[i]) flag |= vadd(v[i]);
+                            if (SUCC(i)) flag |= vadd(v[i]);
                     }
                     __syncthreads();
                     uint32_t sbefore, stotal;
@@ -729,7 +741,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                         }
     #pragma unroll
                         for (int i = 0; i < U; ++i)
-                            if (succ[i]) flag |= vadd(v[i]);
+                            if (SUCC(i)) flag |= vadd(v[i]);
                         __syncthreads();
                     }
                     // a single-row group has distinct targets: no success can repeat a target
@@ -737,7 +749,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     if (multi) {
     #pragma unroll
                         for (int i = 0; i < U; ++i)
-                            if (cand[i] && !succ[i] && vhas(v[i])) flag = true;
+                            if (CAND(i) && !SUCC(i) && vhas(v[i])) flag = true;
                         conflict = __syncthreads_or(flag);
                     }
                     if (!conflict) {
@@ -746,7 +758,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                             uint32_t p = qlen + sbefore;
     #pragma unroll
                             for (int i = 0; i < U; ++i) {
-                                if (succ[i]) q[p + __popc(sm[i] & lt)] = v[i];
+                                if (SUCC(i)) q[p + __popc(sm[i] & lt)] = v[i];
                                 p += __popc(sm[i]);
                             }
                         }
@@ -761,7 +773,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                             uint32_t p = sbefore;
     #pragma unroll
                             for (int i = 0; i < U; ++i) {
-                                if (succ[i]) {
+                                if (SUCC(i)) {
                                     const uint32_t k = p + __popc(sm[i] & lt);
                                     sh.lbuf[k] = gpos + (w * U + i) * 32 + lane;
                                     sh.lbuf[G + k] = v[i];
@@ -773,7 +785,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                         __syncthreads();
     #pragma unroll
                         for (int i = 0; i < U; ++i) {
-                            if (!cand[i] || !vhas(v[i])) continue;
+                            if (!CAND(i) || !vhas(v[i])) continue;
                             const uint32_t pos = gpos + (w * U + i) * 32 + lane;
                             uint32_t minp = 0xffffffffu;
                             for (uint32_t k = 0; k < stotal; ++k)
@@ -784,6 +796,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                         const uint32_t cut = sh.cut;
                         // counts of draws / successes before the cut
                         uint32_t wd2 = 0, ws2 = 0;
+                        uint32_t smk[U];  // the successes kept (sm: all of them, for the rollback)
     #pragma unroll
                         for (int i = 0; i < U; ++i) {
                             const uint32_t a = gpos + (w * U + i) * 32;
@@ -791,7 +804,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                                                 : (cut <= a ? 0u : (cut - a >= 32 ? FULL : ((1u << (cut - a)) - 1u)));
                             wd2 += __popc(dm[i] & keep);
                             ws2 += __popc(sm[i] & keep);
-                            sm[i] &= keep;
+                            smk[i] = sm[i] & keep;
                         }
                         __syncthreads();
                         if (lane == 0) {
@@ -811,8 +824,8 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                         uint32_t p = qlen + s2b;
     #pragma unroll
                         for (int i = 0; i < U; ++i) {
-                            if ((sm[i] >> lane) & 1u) q[p + __popc(sm[i] & lt)] = v[i];
-                            p += __popc(sm[i]);
+                            if ((smk[i] >> lane) & 1u) q[p + __popc(smk[i] & lt)] = v[i];
+                            p += __popc(smk[i]);
                         }
                         qlen += s2t;
                         t += d2t;
@@ -829,12 +842,12 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                                 // committed ones (a repeated target may have shared a bit)
     #pragma unroll
                                 for (int i = 0; i < U; ++i)
-                                    if (succ[i] && gpos + (w * U + i) * 32 + lane >= cut)
+                                    if (SUCC(i) && gpos + (w * U + i) * 32 + lane >= cut)
                                         atomicAnd(&bw[v[i] >> 5], ~(1u << (v[i] & 31)));
                                 __syncthreads();
     #pragma unroll
                                 for (int i = 0; i < U; ++i)
-                                    if ((sm[i] >> lane) & 1u) atomicOr(&bw[v[i] >> 5], 1u << (v[i] & 31));
+                                    if ((smk[i] >> lane) & 1u) atomicOr(&bw[v[i] >> 5], 1u << (v[i] & 31));
                             } else if constexpr (kHash) {
                               if (qlen + sh.hdup + G <= qcap) {
                                 // hash: empty the slots of the post-cut successes (located first, then
@@ -846,7 +859,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                                 uint32_t slot[U];
     #pragma unroll
                                 for (int i = 0; i < U; ++i)
-                                    slot[i] = (succ[i] && gpos + (w * U + i) * 32 + lane >= cut) ? vis.find(v[i])
+                                    slot[i] = (SUCC(i) && gpos + (w * U + i) * 32 + lane >= cut) ? vis.find(v[i])
                                                                                                 : 0xffffffffu;
                                 __syncthreads();
     #pragma unroll
@@ -855,7 +868,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                                 __syncthreads();
     #pragma unroll
                                 for (int i = 0; i < U; ++i)
-                                    if ((sm[i] >> lane) & 1u) vis.add_test(v[i]);
+                                    if ((smk[i] >> lane) & 1u) vis.add_test(v[i]);
                                 if (tid == 0) sh.hdup += s2t;
                             } else {
                                 // rebuild the visited set from the committed members
