@@ -72,15 +72,17 @@ __device__ __forceinline__ bool coin_success(uint64_t s0, uint64_t t, uint64_t t
     return xlo < (uint32_t)tsh;
 }
 
-// High word of the draw (the success test on it alone is exact unless it equals the
-// threshold's high word: callers resolve those rare ties with coin_success).
-__device__ __forceinline__ uint32_t coin_xhi(uint64_t s0, uint64_t t) {
+// High word of the draw before splitmix64's last step (x = z ^ (z >> 31)), zhi.  The last step
+// flips bit 0 of the high word when bit 31 is set, so x < (T << 11) agrees with zhi < thi (thi
+// the threshold's high word) unless zhi ^ thi <= 1: pairs {2k, 2k+1} only straddle an odd thi,
+// and only there (or on equal high words) does the low word matter.  Callers resolve that
+// rare case (2^-31 a draw) with coin_success.
+__device__ __forceinline__ uint32_t coin_zhi(uint64_t s0, uint64_t t) {
     uint64_t z = s0 + t * kGamma;
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
     const uint64_t y = z ^ (z >> 27);
     const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
-    const uint32_t zhi = __umulhi(ylo, 0x133111ebu) + ylo * 0x94d049bbu + yhi * 0x133111ebu;
-    return zhi ^ (zhi >> 31);
+    return __umulhi(ylo, 0x133111ebu) + ylo * 0x94d049bbu + yhi * 0x133111ebu;
 }
 
 // ---------------------------------------------------------------- visited sets ----
@@ -695,20 +697,20 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     uint32_t ws = 0;
                     uint64_t tb = t + dbefore;
                     bool coin[U];
-                    uint32_t tie = 0;
+                    bool tie = false;
     #pragma unroll
                     for (int i = 0; i < U; ++i) {  // branch-free, on the draws' high words
-                        const uint32_t xh = coin_xhi(s0, tb + __popc(dm[i] & lt));
+                        const uint32_t zh = coin_zhi(s0, tb + __popc(dm[i] & lt));
                         const uint32_t th = (uint32_t)(T[i] >> 32);
-                        coin[i] = xh < th;
-                        tie |= (uint32_t)(xh == th) << i;
+                        coin[i] = zh < th;
+                        tie |= (zh ^ th) < 2u;
                         tb += __popc(dm[i]);
                     }
-                    if (__any_sync(FULL, tie)) {  // rare (2^-32 a draw): equal high words, the low words decide
+                    if (__any_sync(FULL, tie)) {  // rare (2^-31 a draw): the low words decide
                         uint64_t tb2 = t + dbefore;
     #pragma unroll
                         for (int i = 0; i < U; ++i) {
-                            if ((tie >> i) & 1u) coin[i] = coin_success(s0, tb2 + __popc(dm[i] & lt), T[i]);
+                            coin[i] = coin_success(s0, tb2 + __popc(dm[i] & lt), T[i]);
                             tb2 += __popc(dm[i]);
                         }
                     }
