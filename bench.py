@@ -90,6 +90,21 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def wait_first(self, timeout: float = 10.0):
+        # nvidia-smi's start-up (driver/NVML init) is slow and can stall the context: let it
+        # finish before the timed region opens, then keep only the samples taken inside it
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        self.rows.clear()
+
+    def ensure_one(self, timeout: float = 1.0):
+        # a timed region shorter than the 200 ms period (config 1) takes the next sample
+        self.late = not self.rows
+        t0 = time.time()
+        while self.proc and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.01)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
@@ -111,8 +126,11 @@ class ClockSampler:
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        out = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": reasons, "samples": len(self.rows)}
+        if getattr(self, "late", False):
+            out["sampled"] = "right after the timed region (shorter than the 200 ms period)"
+        return out
 
 
 def dist_env():
@@ -258,6 +276,7 @@ def run_ours(args, cfg, rank, world, local):
     samples = 0
     results = []
     with ClockSampler(local) as clk:
+        clk.wait_first()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
@@ -271,6 +290,7 @@ def run_ours(args, cfg, rank, world, local):
         with torch.cuda.stream(stream):
             ev1.record(stream)
         ev1.synchronize()
+        clk.ensure_one()
     dev.synchronize()
     torch.cuda.synchronize()
     barrier(world)
