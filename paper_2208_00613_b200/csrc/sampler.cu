@@ -228,6 +228,7 @@ struct SampJob {
     uint32_t* gbits;                 // per-warp global bitmap (GlobBits tier)
     uint32_t qcap;
     int model;
+    int exact_coins;                 // test knob: every coin through the exact (tie) path
     // promotion slots (hash tiers): a sample outgrowing its shared-memory hash takes a slot
     // -- a global visited bitmap (pwords words) and a queue of pqcap members -- and continues
     uint32_t* pbits;
@@ -697,7 +698,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     uint32_t ws = 0;
                     uint64_t tb = t + dbefore;
                     bool coin[U];
-                    bool tie = false;
+                    bool tie = job.exact_coins;
     #pragma unroll
                     for (int i = 0; i < U; ++i) {  // branch-free, on the draws' high words
                         const uint32_t zh = coin_zhi(s0, tb + __popc(dm[i] & lt));
@@ -1066,6 +1067,11 @@ bool promote_enabled() {  // IMMX_NO_PROMOTE=1 restarts overflowing samples on t
     return on;
 }
 
+bool exact_coins_forced() {  // IMMX_EXACT_COINS=1: tests drive every coin through the tie path
+    const char* e = std::getenv("IMMX_EXACT_COINS");
+    return e && *e && *e != '0';
+}
+
 bool debug_tiers() {
     static const bool on = [] {
         const char* e = std::getenv("IMMX_DEBUG_TIERS");
@@ -1208,6 +1214,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     job.cursor = P.cur.p;
     job.ctl = ctl.p;
     job.model = model;
+    job.exact_coins = exact_coins_forced() ? 1 : 0;
 
     const uint32_t* cur_list = nullptr;  // identity
     uint32_t nitems = (uint32_t)count;

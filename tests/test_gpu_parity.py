@@ -384,3 +384,30 @@ def test_device_rmat_c2_matches_golden_graph(im):
         h.update(np.ascontiguousarray(off).tobytes())
         h.update(np.ascontiguousarray(mem).tobytes())
         assert h.hexdigest() == w["sha"]
+
+
+@pytest.fixture
+def exact_coins(monkeypatch):
+    # IMMX_EXACT_COINS=1 routes every coin through the rare exact path (the one taken when the
+    # draw's high word sits within one of the threshold's): bit-exact either way
+    monkeypatch.setenv("IMMX_EXACT_COINS", "1")
+
+
+@pytest.mark.parametrize("model,p", [("wc", 0.0), ("uniform", 0.1), ("uniform", 0.6)])
+def test_sample_exact_coin_path(im, orc, exact_coins, model, p):
+    rng = np.random.default_rng(21)
+    for trial in range(3):
+        g = orc.assign_weights(random_graph(rng, 120 + 60 * trial, 900 + 400 * trial), model, p)
+        gt = orc.transpose(g)
+        a = orc.sample_block(gt, 600, 7 * trial, 77 + trial)
+        b = sample_dev(im, gt, 600, 7 * trial, 77 + trial)
+        assert_same_sets(a[0], a[1], b[0], b[1])
+
+
+def test_c2_samples_exact_coin_path(im, orc, exact_coins):
+    g = im.generate_rmat(18, 16, 0.57, 0.19, 0.19, 1)
+    im.assign_weights_f32(g, "uniform", 0.01)
+    gt = orc.transpose(csr_of(g))
+    a = orc.sample_block(gt, 120, 1000, 42)
+    b = sample_dev(im, gt, 120, 1000, 42)
+    assert_same_sets(a[0], a[1], b[0], b[1])
