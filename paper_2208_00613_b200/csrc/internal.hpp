@@ -127,6 +127,9 @@ struct Device {
     // do not pay first-touch page faults on ~100 MB of fresh host memory
     std::shared_ptr<struct HostCodebook> run_cb;
     std::vector<unsigned long long> run_lut;
+    // mean RRR set size last seen on a graph (sizes a cold pool's arena without a pilot batch)
+    const void* seen_graph = nullptr;
+    double seen_mean = 0.0;
 };
 
 struct DevGraph {

@@ -1112,9 +1112,12 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     if (count > 0xffffffffULL) fail(IMMX_EINVAL, "sample batch larger than 2^32");
     if (G.n == 0) fail(IMMX_EINVAL, "graph has no vertices");
     if (model == IMMX_MODEL_LT && !G.has_lt) fail(IMMX_EINVAL, "LT model requires per-edge LT weights");
-    if (P.count < 1024 && count > 8192) {
-        // cold pool: a pilot batch measures the mean set size, so the arena is sized once
-        // (an undersized arena makes in-flight samples redo their work)
+    // mean set size: the pool's, else the last one seen on this graph on this device
+    const bool known = d.seen_graph == (const void*)&G && d.seen_mean > 0.0;
+    if (P.count < 1024 && count > 8192 && !known) {
+        // cold pool on a new graph: a pilot batch measures the mean set size, so the arena is
+        // sized once (an undersized arena makes in-flight samples redo their work); repeated
+        // runs on the graph size it from the last mean and skip the pilot's launch tail
         sample_into_pool(P, G, 2048, first, seed, d_roots, d_states, model);
         sample_into_pool(P, G, count - 2048, first + 2048, seed, d_roots ? d_roots + 2048 : nullptr,
                          d_states ? d_states + 2048 : nullptr, model);
@@ -1124,7 +1127,8 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     P.off.reserve(base + count, s);
     P.len.reserve(base + count, s);
     // arena: grow to an estimate (mean size so far, else 64 per sample)
-    const double mean = P.count ? (double)P.members / (double)P.count : (double)std::min<uint64_t>(G.n, 4096);
+    const double mean = P.count ? (double)P.members / (double)P.count
+                                : (known ? d.seen_mean : (double)std::min<uint64_t>(G.n, 4096));
     const uint64_t want = P.arena_used + (uint64_t)(mean * 1.25 * (double)count) + 4096;
     P.arena.reserve(want, s);
     P.cur.reserve(1, s);
@@ -1324,6 +1328,10 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     P.count = base + count;
     P.members += members;
     P.edges += edges;
+    if (P.count >= 1024) {
+        d.seen_graph = &G;
+        d.seen_mean = (double)P.members / (double)P.count;
+    }
 }
 
 }  // namespace immx_dev
