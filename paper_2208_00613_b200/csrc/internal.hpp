@@ -1,5 +1,7 @@
 // internal.hpp -- device-side objects behind the C-ABI handles (not exported).
 #pragma once
+
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -128,12 +130,18 @@ struct Device {
     std::shared_ptr<struct HostCodebook> run_cb;
     std::vector<unsigned long long> run_lut;
     // mean RRR set size last seen on a graph (sizes a cold pool's arena without a pilot batch)
-    const void* seen_graph = nullptr;
+    uint64_t seen_graph = 0;  // DevGraph::uid
     double seen_mean = 0.0;
 };
 
+inline uint64_t next_graph_uid() {  // identity of a device graph (sampler caches key on it)
+    static std::atomic<uint64_t> c{0};
+    return ++c;
+}
+
 struct DevGraph {
     Device* dev = nullptr;
+    uint64_t uid = next_graph_uid();
     uint64_t n = 0, m = 0;
     DBuf<uint64_t> row;  // n+1   (reverse CSR offsets)
     DBuf<uint32_t> col;  // m     (reverse CSR targets)

@@ -1113,7 +1113,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     if (G.n == 0) fail(IMMX_EINVAL, "graph has no vertices");
     if (model == IMMX_MODEL_LT && !G.has_lt) fail(IMMX_EINVAL, "LT model requires per-edge LT weights");
     // mean set size: the pool's, else the last one seen on this graph on this device
-    const bool known = d.seen_graph == (const void*)&G && d.seen_mean > 0.0;
+    const bool known = d.seen_graph == G.uid && d.seen_mean > 0.0;
     if (P.count < 1024 && count > 8192 && !known) {
         // cold pool on a new graph: a pilot batch measures the mean set size, so the arena is
         // sized once (an undersized arena makes in-flight samples redo their work); repeated
@@ -1329,7 +1329,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     P.members += members;
     P.edges += edges;
     if (P.count >= 1024) {
-        d.seen_graph = &G;
+        d.seen_graph = G.uid;
         d.seen_mean = (double)P.members / (double)P.count;
     }
 }

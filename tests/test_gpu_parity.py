@@ -411,3 +411,4 @@ def test_c2_samples_exact_coin_path(im, orc, exact_coins):
     a = orc.sample_block(gt, 120, 1000, 42)
     b = sample_dev(im, gt, 120, 1000, 42)
     assert_same_sets(a[0], a[1], b[0], b[1])
+
