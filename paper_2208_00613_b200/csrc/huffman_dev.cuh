@@ -11,24 +11,30 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 
 
 
 // ---- bit reader over one set's stream -------------------------------------------
+// The word after the buffered ones is loaded one refill ahead (pf), so a refill does not
+// wait on memory: the stream's loads overlap the decoding of the buffered codewords.  (Reads
+// run up to three words past a stream's end; the store keeps 4 words of padding.)
 struct BitReader {
     const uint32_t* w;
     uint64_t buf;
     uint32_t nb;     // valid bits in buf (MSB-aligned)
-    uint32_t next;   // next word to load
+    uint32_t next;   // index of the word held in pf
+    uint32_t pf;     // prefetched next word
     __device__ void init(const uint32_t* words) {
         w = words;
         buf = 0;
         nb = 0;
         next = 0;
+        pf = __ldg(w);
         refill();
         refill();
     }
     __device__ __forceinline__ void refill() {
         if (nb <= 32) {
-            buf |= (uint64_t)bswap32(__ldg(w + next)) << (32 - nb);
+            buf |= (uint64_t)bswap32(pf) << (32 - nb);
             nb += 32;
             next++;
+            pf = __ldg(w + next);
         }
     }
     __device__ __forceinline__ uint32_t peek(uint32_t W) const { return (uint32_t)(buf >> (64 - W)); }
