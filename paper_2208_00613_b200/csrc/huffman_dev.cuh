@@ -20,14 +20,13 @@ struct BitReader {
     uint32_t nb;     // valid bits in buf (MSB-aligned)
     uint32_t next;   // index of the word held in pf
     uint32_t pf;     // prefetched next word
-    __device__ void init(const uint32_t* words) {
+    __device__ void init(const uint32_t* words) {  // (three independent loads)
         w = words;
-        buf = 0;
-        nb = 0;
-        next = 0;
-        pf = __ldg(w);
-        refill();
-        refill();
+        const uint32_t a = __ldg(w), b = __ldg(w + 1);
+        pf = __ldg(w + 2);
+        buf = ((uint64_t)bswap32(a) << 32) | bswap32(b);
+        nb = 64;
+        next = 2;
     }
     __device__ __forceinline__ void refill() {
         if (nb <= 32) {

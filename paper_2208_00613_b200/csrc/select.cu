@@ -128,7 +128,7 @@ __device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict
     bool active = false, fresh = false;
     uint32_t j = 0, pos = 0, nbits = 0, nd = 0, base = 0, lim = 0xffffffffu;
     bool seg0 = false;
-    uint64_t item = 0;
+    uint64_t item = 0, wo = 0;
     BitReader br;
     for (;;) {
         uint32_t idle = __ballot_sync(FULL, !active);
@@ -147,16 +147,45 @@ __device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict
                 }
                 const uint64_t i = cur + lane;
                 const uint32_t it = i < hi ? srcs.at(i) : 0u;
-                const bool lv = i < hi && op.live(sv.set_of(it));
+                // the candidate's segment metadata is read alongside its live flag (independent
+                // loads) and handed over with the item, so opening it waits on the stream only
+                const uint32_t jc = sv.set_of(it);
+                const bool lv = i < hi && op.live(jc);
+                uint32_t cbits = 0, cbit0 = 0, cbase = 0, clim = 0xffffffffu;
+                uint64_t cwo = 0;
+                if (i < hi) {
+                    cbits = sv.bits[jc];
+                    cwo = sv.woff[jc];
+                    if (it < sv.count) {
+                        clim = sv.segd[jc] ? kSegCodewords : 0xffffffffu;
+                    } else {
+                        const uint64_t x = it - sv.count;
+                        cbit0 = sv.xbit[x];
+                        cbase = (uint32_t)(x - sv.xfirst[jc] + 1) * kSegCodewords;
+                        clim = kSegCodewords;
+                    }
+                }
                 const uint32_t L = __ballot_sync(FULL, lv);
                 const uint32_t take = min(__popc(L), __popc(idle));
                 const uint32_t r = __popc(idle & lt);
                 const bool assign = !active && r < take;
                 const uint32_t src = assign ? nth_set_bit(L, r) : lane;
                 const uint32_t isrc = __shfl_sync(FULL, it, src);
+                const uint32_t jsrc = __shfl_sync(FULL, jc, src);
+                const uint32_t bsrc = __shfl_sync(FULL, cbits, src);
+                const uint32_t b0src = __shfl_sync(FULL, cbit0, src);
+                const uint32_t basesrc = __shfl_sync(FULL, cbase, src);
+                const uint32_t limsrc = __shfl_sync(FULL, clim, src);
+                const uint64_t wosrc = __shfl_sync(FULL, cwo, src);
                 if (assign) {
                     item = isrc;
                     active = fresh = true;
+                    j = jsrc;
+                    nbits = bsrc;
+                    pos = b0src;
+                    base = basesrc;
+                    lim = limsrc;
+                    wo = wosrc;
                 }
                 if (out_list) {  // the taken items are the next round's candidates
                     const uint32_t A = __ballot_sync(FULL, assign);
@@ -173,26 +202,12 @@ __device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict
             if (drained) break;
             continue;
         }
-        if (fresh) {  // newly assigned: open the segment
-            uint32_t bit0 = 0;
-            if (item < sv.count) {
-                j = (uint32_t)item;
-                seg0 = true;
-                base = 0;
-                lim = sv.segd[j] ? kSegCodewords : 0xffffffffu;
-            } else {
-                const uint64_t x = item - sv.count;
-                j = sv.xset[x];
-                seg0 = false;
-                bit0 = sv.xbit[x];
-                base = (uint32_t)(x - sv.xfirst[j] + 1) * kSegCodewords;
-                lim = kSegCodewords;
-            }
-            nbits = sv.bits[j];
+        if (fresh) {  // newly assigned: open the segment (metadata came with the item)
+            const uint32_t bit0 = pos;
+            seg0 = item < sv.count;
             if (nbits == kDenseBits) nbits = 0;  // hybrid bitmap sets: the k_dense_* passes
-            br.init(sv.words + sv.woff[j] + (bit0 >> 5));
+            br.init(sv.words + wo + (bit0 >> 5));
             if (bit0 & 31) br.skip(bit0 & 31);
-            pos = bit0;
             nd = 0;
             fresh = false;
         }
