@@ -9,9 +9,12 @@
 // work counter).  The flattened edge sequence of a batch of rows is consumed in groups of
 // NW*32*U edges decided from the visited snapshot at the group start, with CTA prefixes of
 // per-warp draw counts giving every lane its draw numbers; groups that span rows resolve
-// repeated targets exactly (see the block comment further down).  Visited set: a
-// shared-memory bitmap over all n when it fits (c1, c2); else a shared-memory hash whose
-// samples move in place to a promotion slot (a global bitmap + queue) at half its capacity;
+// repeated targets exactly (see the block comment further down).  The coins are decided on
+// one 32-bit word of the draw (coin_zhi), ties resolved exactly behind a warp vote; per-lane
+// candidate / success flags are bits of the warps' ballot masks.  The kernel is bound by the
+// integer-ALU pipe.  Visited set: a shared-memory bitmap over all n when
+// it fits (c1, c2); else a shared-memory hash behind a one-hash bit filter, whose samples move
+// in place to a promotion slot (a global bitmap + queue) at half its capacity;
 // without a free slot, or past the slot's queue, a sample restarts -- the stream is a pure
 // function of (seed, index) -- on a 128 KB hash tier and then a per-CTA global bitmap.
 //
