@@ -11,6 +11,7 @@
 #include <cstdlib>
 
 #include <chrono>
+#include <future>
 #include <memory>
 #include <cmath>
 #include <cstring>
@@ -882,6 +883,8 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         }
         int mode = IMMX_MODE_RAW, char_mode = IMMX_MODE_RAW;
         double t_codebook = 0.0, t_lut = 0.0;  // host: Huffman tree, decode table
+        std::future<void> lut_job;             // the decode table, built beside the encode
+        uint32_t lut_rb = 1;
         double skew = 0.0, dens = 0.0;
         if (!d.run_cb) d.run_cb = std::make_shared<HostCodebook>();
         HostCodebook& cb = *d.run_cb;
@@ -925,21 +928,20 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     if (std::getenv("IMMX_DEBUG_CODEBOOK"))
                         std::fprintf(stderr, "[immx codebook] coded %llu leaves (device sort + D2H) %.4f s, tree+codes %.4f s\n",
                                      (unsigned long long)leaves.size(), t_leaves, t_codebook - t_leaves);
-                    const auto tl = Clock::now();
-                    std::vector<unsigned long long>& lut = d.run_lut;
-                    uint32_t rb = 1;
-                    build_decode_lut(cb, lut, rb);
-                    t_lut = secs(tl);
-                    if (std::getenv("IMMX_DEBUG_CODEBOOK"))
-                        std::fprintf(stderr, "[immx codebook] decode table %zu entries (root %u bits) %.4f s, nodes %zu\n",
-                                     lut.size(), rb, t_lut, cb.nodes.size());
+                    // the decode table is needed only by the selection: build it on a host
+                    // thread while the device encodes the blocks
+                    lut_job = std::async(std::launch::async, [&cb, &d, &lut_rb, &t_lut, secs]() {
+                        const auto tl = Clock::now();
+                        build_decode_lut(cb, d.run_lut, lut_rb);
+                        t_lut = secs(tl);
+                    });
                     if (!d.run_store) d.run_store = new immx_store;
                     store = d.run_store;
                     store->s.count = store->s.total_words = store->s.total_copied = store->s.payload_bytes = 0;
                     store->s.dense_count = 0;
                     store->s.n_extra = 0;
                     store->s.hybrid = mode == IMMX_MODE_HYBRID;
-                    store_set_leaf_codes(store->s, d, n, cb, lut, rb);
+                    store_set_leaf_codes(store->s, d, n, cb, {}, 1);
                 } else if (mode == IMMX_MODE_BITMAP) {
                     bm.reset(new immx_bitmap);
                     bm->b.dev = &d;
@@ -982,6 +984,14 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         double uncoded = 0.0;
         if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {
             uncoded = (double)count_uncoded_dev(d, hist.p, store->s.code_len.p, n) / (double)n;
+        }
+
+        if (lut_job.valid()) {
+            lut_job.get();
+            store_set_lut(store->s, d, d.run_lut, lut_rb);
+            if (std::getenv("IMMX_DEBUG_CODEBOOK"))
+                std::fprintf(stderr, "[immx codebook] decode table %zu entries (root %u bits) %.4f s, nodes %zu\n",
+                             d.run_lut.size(), lut_rb, t_lut, cb.nodes.size());
         }
 
         // ---- selection (pipeline.cpp:156-175) ----

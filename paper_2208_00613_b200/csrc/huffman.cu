@@ -288,6 +288,15 @@ void store_set_leaf_codes(Store& S, Device& d, uint64_t n, const HostCodebook& c
     CK(cudaStreamSynchronize(s));
 }
 
+void store_set_lut(Store& S, Device& d, const std::vector<unsigned long long>& lut, uint32_t root_bits) {
+    cudaStream_t s = d.stream;
+    S.lut.exact(std::max<uint64_t>(lut.size(), 1));
+    if (!lut.empty()) CK(cudaMemcpyAsync(S.lut.p, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice, s));
+    S.lut_root_bits = root_bits;
+    S.lut_entries = lut.size();
+    CK(cudaStreamSynchronize(s));  // (the host vector may change after the call)
+}
+
 uint64_t count_uncoded_dev(Device& d, const unsigned int* d_hist, const uint8_t* d_code_len, uint64_t n) {
     cudaStream_t s = d.stream;
     unsigned long long* out = d.scal.p + 28;

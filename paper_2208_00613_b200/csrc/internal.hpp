@@ -266,6 +266,7 @@ struct HostCodebook;
 // the codes of the coded vertices only (scattered on the device; every other vertex uncoded)
 void store_set_leaf_codes(Store& S, Device& d, uint64_t n, const HostCodebook& cb,
                           const std::vector<unsigned long long>& lut, uint32_t root_bits);
+void store_set_lut(Store& S, Device& d, const std::vector<unsigned long long>& lut, uint32_t root_bits);
 // vertices counted in the table (hist > 0) that have no code
 uint64_t count_uncoded_dev(Device& d, const unsigned int* d_hist, const uint8_t* d_code_len, uint64_t n);
 void store_set_codes(Store& S, Device& d, uint64_t n, const uint64_t* code_bits, const uint8_t* code_len,
