@@ -267,11 +267,12 @@ def run_ours(args, cfg, rank, world, local):
     for _ in range(args.warmup):
         one_step()
     dev.synchronize()
-    # each nvidia-smi query can stall the driver for tens of ms, which distorts a short timed
-    # region (configs 1 and 3 run ~10-50 ms steps): regions expected under 2 s are sampled
-    # every 2 s -- in practice right after the region -- longer ones every 200 ms
+    # each nvidia-smi query can stall the driver for tens of ms (measured: 29 queries at 200 ms
+    # cost config 2 +140 ms a step on one box), which distorts the timed region: regions
+    # expected under 2 s are sampled every 2 s -- in practice right after the region --, longer
+    # ones once a second (5+ samples inside config 2's region)
     expect_s = (time.perf_counter() - tw) / max(args.warmup, 1) * args.steps
-    period_ms = 200 if expect_s >= 2.0 else 2000
+    period_ms = 1000 if expect_s >= 2.0 else 2000
 
     # ---- timed: graph resident in HBM ----
     dev.profile(True)
