@@ -232,6 +232,8 @@ struct SampJob {
     uint32_t qcap;
     int model;
     int exact_coins;                 // test knob: every coin through the exact (tie) path
+    unsigned int* run_hist;          // non-null: the pool's running vertex histogram (select_raw's),
+                                     // counted as the sets are committed
     // promotion slots (hash tiers): a sample outgrowing its shared-memory hash takes a slot
     // -- a global visited bitmap (pwords words) and a queue of pqcap members -- and continues
     uint32_t* pbits;
@@ -312,7 +314,10 @@ __global__ void __launch_bounds__(256) rrr_kernel(GView g, SampJob job, uint32_t
             if (base + res.size > job.arena_cap) {
                 if (lane == 0) job.nospace_list[atomicAdd(&job.ctl->n_nospace, 1u)] = j;
             } else {
-                for (uint32_t i = lane; i < res.size; i += 32) job.arena[base + i] = q[i];
+                for (uint32_t i = lane; i < res.size; i += 32) {
+                    job.arena[base + i] = q[i];
+                    if (job.run_hist) atomicAdd(&job.run_hist[q[i]], 1u);
+                }
                 if (lane == 0) {
                     job.set_off[job.pool_base + j] = base;
                     job.set_len[job.pool_base + j] = res.size;
@@ -939,7 +944,11 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
             if (base + qlen > job.arena_cap) {
                 if (tid == 0) job.nospace_list[atomicAdd(&job.ctl->n_nospace, 1u)] = j;
             } else {
-                for (uint32_t k = tid; k < qlen; k += blockDim.x) job.arena[base + k] = q[k];
+                for (uint32_t k = tid; k < qlen; k += blockDim.x) {
+                    const uint32_t v = q[k];
+                    job.arena[base + k] = v;
+                    if (job.run_hist) atomicAdd(&job.run_hist[v], 1u);
+                }
                 if (tid == 0) {
                     job.set_off[job.pool_base + j] = base;
                     job.set_len[job.pool_base + j] = qlen;
@@ -1222,6 +1231,15 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     job.ctl = ctl.p;
     job.model = model;
     job.exact_coins = exact_coins_forced() ? 1 : 0;
+    // select_raw's running histogram of this pool, when it already covers exactly the sets
+    // before this batch: the sampler counts the batch into it (no separate pass over the sets).
+    // Only for large sets (mean >= 64: c2 -14 ms a run); with many small ones (c4) the
+    // commits' atomics cost more than the pass they replace.
+    job.run_hist = nullptr;
+    RawIndex* rx = P.rix.get();
+    const bool fuse_hist = rx && rx->epoch == P.epoch && rx->n == G.n && rx->hist_upto == base && rx->hist.p &&
+                           P.count && P.members >= 64 * P.count;
+    if (fuse_hist) job.run_hist = rx->hist.p;
 
     const uint32_t* cur_list = nullptr;  // identity
     uint32_t nitems = (uint32_t)count;
@@ -1328,6 +1346,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     CK(cudaMemcpyAsync(&cursor, P.cur.p, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     P.arena_used = cursor;
+    if (fuse_hist) rx->hist_upto = base + count;
     P.count = base + count;
     P.members += members;
     P.edges += edges;
