@@ -915,13 +915,11 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                 char_mode = choose_encoding_host(skew, dens);
                 mode = cfg->mode >= 0 ? cfg->mode : char_mode;
                 if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {
-                    DBuf<unsigned int> h1;
-                    h1.exact(n);
-                    CK(cudaMemsetAsync(h1.p, 0, n * 4, st));
-                    pool_hist_dev(pool, lo, hi, h1.p);
+                    // block 1's table is also the encode-time table after block 1 (counted once)
+                    pool_hist_dev(pool, lo, hi, hist.p);
                     const auto tc = Clock::now();
                     std::vector<unsigned long long> leaves;
-                    codebook_leaves_dev(d, h1.p, n, leaves);
+                    codebook_leaves_dev(d, hist.p, n, leaves);
                     const double t_leaves = secs(tc);
                     build_codebook_sorted(leaves.data(), leaves.size(), n, cb);
                     t_codebook = secs(tc);
@@ -950,7 +948,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
             }
             uint64_t enc = 0;
             if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {  // pipeline.cpp:106-118
-                pool_hist_dev(pool, lo, hi, hist.p);
+                if (i != 1) pool_hist_dev(pool, lo, hi, hist.p);  // (block 1: counted above)
                 unsigned long long* key = d.scal.p + 60;
                 CK(cudaMemsetAsync(key, 0, 8, st));
                 argmax_dev(d, hist.p, n, key);
