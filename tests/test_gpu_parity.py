@@ -412,3 +412,16 @@ def test_c2_samples_exact_coin_path(im, orc, exact_coins):
     b = sample_dev(im, gt, 120, 1000, 42)
     assert_same_sets(a[0], a[1], b[0], b[1])
 
+
+
+def test_sample_exact_coin_path_per_edge(im, orc, exact_coins):
+    # per-edge thresholds: the exact path re-derives each position's threshold from its row
+    rng = np.random.default_rng(13)
+    g = random_graph(rng, 300, 5000)
+    pr = rng.choice([0.0, 1.0, 1e-12, 0.3, 0.7, 0.999], size=g.m)
+    from oracle.oracle import CSR
+    g = CSR(g.n, g.off, g.tgt, pr.astype(np.float64))
+    gt = orc.transpose(g)
+    a = orc.sample_block(gt, 1500, 0, 11)
+    b = sample_dev(im, gt, 1500, 0, 11)
+    assert_same_sets(a[0], a[1], b[0], b[1])
