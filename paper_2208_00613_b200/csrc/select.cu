@@ -525,20 +525,47 @@ __global__ void k_raw_scan_mark(const uint32_t* __restrict__ arena, const uint64
             ctl->live_snap = ctl->live_vol;
         }
     }
+    // A warp takes 32 consecutive sets (coalesced flags and offsets): each lane scans its own
+    // set when it is small; sets above 16 members are scanned by the whole warp, one by one.
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
     const uint64_t w = gt >> 5, nw = gs >> 5;
     unsigned long long hv = 0;
-    for (uint64_t j = w; j < count; j += nw) {
-        if (covered[j]) continue;
-        const uint64_t b = off[j];
-        const uint32_t l = len[j];
-        bool found = false;
-        for (uint32_t i0 = 0; i0 < l && !found; i0 += 32)
-            found = __any_sync(FULL, i0 + lane < l && arena[b + i0 + lane] == pick);
-        if (found && lane == 0) {
-            covered[j] = r + 1;
-            hitlist[atomicAdd(&ctl->nhit, 1ull)] = (uint32_t)j;
-            hv += l;
+    for (uint64_t j0 = w * 32; j0 < count; j0 += nw * 32) {
+        const uint64_t j = j0 + lane;
+        uint64_t b = 0;
+        uint32_t l = 0;
+        bool mine = false, big = false;
+        if (j < count && !covered[j]) {
+            b = off[j];
+            l = len[j];
+            big = l > 16;
+            if (!big)
+                for (uint32_t i = 0; i < l; ++i)
+                    if (arena[b + i] == pick) {
+                        mine = true;
+                        break;
+                    }
+        }
+        for (uint32_t bm = __ballot_sync(FULL, big); bm; bm &= bm - 1) {
+            const uint32_t src = __ffs(bm) - 1;
+            const uint64_t bb = __shfl_sync(FULL, b, src);
+            const uint32_t ll = __shfl_sync(FULL, l, src);
+            bool found = false;
+            for (uint32_t i0 = 0; i0 < ll && !found; i0 += 32)
+                found = __any_sync(FULL, i0 + lane < ll && arena[bb + i0 + lane] == pick);
+            if (found && lane == src) mine = true;
+        }
+        const uint32_t hm = __ballot_sync(FULL, mine);
+        if (hm) {
+            unsigned long long h0 = 0;
+            if (lane == 0) h0 = atomicAdd(&ctl->nhit, (unsigned long long)__popc(hm));
+            h0 = __shfl_sync(FULL, h0, 0);
+            if (mine) {
+                covered[j] = r + 1;
+                hitlist[h0 + __popc(hm & lt)] = (uint32_t)j;
+                hv += l;
+            }
         }
     }
     warp_add_u64(&ctl->hvol, hv);
