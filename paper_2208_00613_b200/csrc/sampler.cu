@@ -14,7 +14,7 @@
 // candidate / success flags are bits of the warps' ballot masks.  The kernel is bound by the
 // integer-ALU pipe.  Visited set: a shared-memory bitmap over all n when
 // it fits (c1, c2); else a shared-memory hash behind a one-hash bit filter, whose samples move
-// in place to a promotion slot (a global bitmap + queue) at 3/4 of its capacity;
+// in place to a promotion slot (a global bitmap + queue) at 7/8 of its capacity;
 // without a free slot, or past the slot's queue, a sample restarts -- the stream is a pure
 // function of (seed, index) -- on a 128 KB hash tier and then a per-CTA global bitmap.
 //
@@ -575,10 +575,11 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
             };
             while (qhead < qlen && !overflow) {
                 if constexpr (kHash && !P) {
-                    // at 3/4 of the hash's capacity (3/8 load; the bit filter keeps the longer
+                    // at 7/8 of the hash's capacity (7/16 load; the bit filter keeps the longer
                     // chains off most probes): continue in a promotion slot (uniform test).
-                    // (Half: c5 IMM 4.52 s; 3/4: 4.35 s; later, groups overflow and restart.)
-                    if (job.npslots && !no_slot && qlen + sh.hdup > qcap / 4 * 3) {
+                    // (c5 IMM: at 1/2 4.52 s, 5/8 4.39, 3/4 4.34, 7/8 4.30; at capacity - 64
+                    // groups overflow and restart: 4.65 s)
+                    if (job.npslots && !no_slot && qlen + sh.hdup > qcap / 8 * 7) {
                         want_promote = true;
                         return;
                     }
