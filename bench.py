@@ -1,16 +1,18 @@
 """Benchmark of the B200 IMM hot path (one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], the metric's config): directed R-MAT scale 18, edge
-factor 16, (a,b,c,d)=(0.57,0.19,0.19,0.05), generator seed 1, duplicates and self-loops
-removed; IC with uniform p = fl32(0.01); IMM k=50, epsilon=0.5, 8 blocks, Huffman
-encoding, sampling seed 42.  Synthetic data: the paper's SNAP/LAW graphs are not available.
+Workload (default): BASELINE.json configs[4] (c5), the largest single-GPU config -- BASELINE's
+metric names no config, so the N=1 line is quoted on the largest one: directed R-MAT scale 25
+(33.5 M vertices), edge factor 42 (1.37 B edges after dedup), (a,b,c,d)=(0.57,0.19,0.19,0.05),
+generator seed 4, weighted-cascade IC fl32(1/indeg(v)), IMM k=50, epsilon=0.5, 8 blocks,
+per-set hybrid store (Huffman; bitmap for sets above n/32), sampling seed 42.  `--config
+c1..c4` runs the others.  Synthetic data: the paper's SNAP/LAW graphs are not available.
 
 A step = one full IMM run (theta estimation -> sampling + learn-then-compress encoding ->
 greedy selection on the compressed store).  `value` = RRR samples materialised per second
 of the step, graph resident in HBM; `e2e` = the same through the C-ABI from pinned host
 buffers (forward graph H2D + device transpose + run + results D2H inside the timed region).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
 N > 1: one process per GPU under torchrun; replicas only (the path has no data exchange at
 this tier), value = samples of all ranks / max-over-ranks time.
@@ -32,19 +34,22 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: (generator, weights, k, eps, blocks, mode, description)
-    "c1": dict(gen=("er", 10000, 100000, 0), weights=("wc", 0.0), k=10, eps=0.5, blocks=10, mode="huffman",
+    "c1": dict(gen=("er", 10000, 100000, 0), weights=("wc", 0.0), k=10, eps=0.5, blocks=10, mode="huffman", ref_samples=20000,
                desc="ER n=10k m=100k seed 0, WC fl32, k=10 eps=0.5 b=10 huffman"),
-    "c2": dict(gen=("rmat", 18, 16, 1), weights=("uniform", 0.01), k=50, eps=0.5, blocks=8, mode="huffman",
+    "c2": dict(gen=("rmat", 18, 16, 1), weights=("uniform", 0.01), k=50, eps=0.5, blocks=8, mode="huffman", ref_samples=20000,
                desc="R-MAT scale 18 EF16 (.57,.19,.19) seed 1, IC p=fl32(0.01), k=50 eps=0.5 b=8 huffman"),
     "c3": dict(gen=("rmat", 20, 16, 2), weights=("wc", 0.0), k=100, eps=0.5, blocks=8, mode="hybrid",
                desc="R-MAT scale 20 EF16 seed 2, LT (in-weights U(0,1) normalised, f32, seed 3), k=100 eps=0.5 b=8 "
-                    "per-set hybrid (bitmap above n/32, Huffman otherwise)", device_gen=True, lt_seed=3),
+                    "per-set hybrid (bitmap above n/32, Huffman otherwise)", device_gen=True, lt_seed=3,
+               ref_samples=20000),
     "c4": dict(gen=("rmat", 22, 24, 3), weights=("wc", 0.0), k=100, eps=0.13, blocks=8, mode="huffman",
-               desc="R-MAT scale 22 EF24 seed 3, WC fl32, k=100 eps=0.13 b=8 huffman", device_gen=True),
+               desc="R-MAT scale 22 EF24 seed 3, WC fl32, k=100 eps=0.13 b=8 huffman", device_gen=True,
+               ref_samples=20000),
     "c5": dict(gen=("rmat", 25, 42, 4), weights=("wc", 0.0), k=50, eps=0.5, blocks=8, mode="hybrid",
                desc="R-MAT scale 25 EF42 seed 4, WC fl32, k=50 eps=0.5 b=8 per-set hybrid (bitmap above n/32, "
-                    "Huffman otherwise)", device_gen=True),
+                    "Huffman otherwise)", device_gen=True, ref_samples=4000),
 }
+DTYPE = "u32/u64 integer (RNG u64, ids u32)"
 METRIC = "RRR samples/s & achieved HBM GB/s at 1 B200; IMM end-to-end s; compress ratio"
 SEED = 42
 
@@ -170,53 +175,105 @@ def barrier(world):
 
 
 # ------------------------------------------------------------------ CPU arms
-def cpu_reference_rate(g_arrays, n, samples: int, first: int, threads: int, transposed: bool = False):
-    """The unmodified reference (oracle/_ref, compiled from its sources) sampling
-    `samples` RRR sets of the workload with `threads` OpenMP workers -> (samples/s, seconds)."""
-    from oracle.oracle import CSR, RefLib
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
-    off, tgt, pr = g_arrays
-    ref = RefLib()
-    rg = ref.graph(CSR(n, off, tgt, pr))
-    rgt = rg if transposed else rg.transpose()
-    t0 = time.perf_counter()
-    rgt.sample_block(samples, first, SEED, threads)
-    dt = time.perf_counter() - t0
-    return samples / dt, dt
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class ReferenceWindow:
+    """The reference's CPU sampling path on the workload's graph, loaded from oracle/ only.
+
+    IC configs: the unmodified reference (oracle/_ref/libimmx_ref.so, built from its sources
+    with OpenMP) -- G^T is generated inside that library by oracle/gen_graph.c (the same
+    definition as the product's device generator, pinned by tests/test_gen_oracle.py and the
+    graph SHA-256 goldens), and `sample_block` (sampler.cpp:85-104, the ~99% phase of the
+    reference IMM on these configs) samples windows of global indices with all host threads.
+    LT (c3): the reference has no LT sampler, so the C restatement's LT walk
+    (oracle/liboracle.so oc_sample_block_lt, one thread) is the "port" baseline.
+    No product code is loaded on this path."""
+
+    def __init__(self, cfg):
+        self.cfg = cfg
+        self.lt = "lt_seed" in cfg
+        t0 = time.perf_counter()
+        if self.lt:
+            from oracle.oracle import Oracle
+
+            self.orc = Oracle()
+            self.g, self.w = self.orc.generate(cfg["gen"], cfg["weights"], reverse=True, lt_seed=cfg["lt_seed"])
+            self.kind, self.threads = "port", 1
+        else:
+            from oracle.oracle import RefLib
+
+            self.g = RefLib().generate(cfg["gen"], cfg["weights"], reverse=True)
+            self.kind, self.threads = "reference", host_cores()
+        self.gen_s = time.perf_counter() - t0
+
+    def sample(self, count: int, first: int) -> float:
+        t0 = time.perf_counter()
+        if self.lt:
+            self.orc.sample_block_lt(self.g, self.w, count, first, SEED)
+        else:
+            self.g.sample_block(count, first, SEED, self.threads)
+        return time.perf_counter() - t0
+
+    def describe(self, count: int, steps: int, first: int, seconds: float) -> dict:
+        what = ("reference sample_block (oracle/_ref, unmodified sources, OpenMP)" if not self.lt else
+                "C-restatement LT walk oc_sample_block_lt (the reference has no LT path)")
+        return {"kind": self.kind, "cores": self.threads, "cpu_model": cpu_model(),
+                "sample": f"{what}: {steps} x {count} RRR sets of the workload, global indices from {first}, "
+                          f"{seconds:.1f} s; graph generated by oracle/gen_graph.c in {self.gen_s:.1f} s (untimed)"}
 
 
 def run_reference_arm(args, cfg, rank, world):
     if rank != 0:
         return 0
-    import paper_2208_00613_b200 as im  # only the host generator (same synthetic graph)
-
-    g = make_graph(im, cfg)
-    off, tgt, pr, _ = g.arrays()
-    threads = os.cpu_count() or 1
-    per_step = args.ref_samples
-    # warm-up steps, then K timed steps over consecutive index windows of the workload
+    per_step = args.ref_samples or cfg["ref_samples"]
+    rw = ReferenceWindow(cfg)
     idx = 0
     for _ in range(args.warmup):
-        cpu_reference_rate((off, tgt, pr), g.n, per_step, idx, threads)
+        rw.sample(per_step, idx)
         idx += per_step
+    first = idx
     t = 0.0
     for _ in range(args.steps):
-        _, dt = cpu_reference_rate((off, tgt, pr), g.n, per_step, idx, threads)
-        t += dt
+        t += rw.sample(per_step, idx)
         idx += per_step
     value = per_step * args.steps / t
+    cpu = {"value": value, "unit": "samples/s", **rw.describe(per_step, args.steps, first, t)}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer", "data": "synthetic",
-        "config": {"workload": args.config, "desc": cfg["desc"], "step": f"reference sample_block of {per_step} RRR "
-                   "sets (sampling is ~99% of the reference IMM time on this config, SURVEY §3.1)"},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "reference",
-                         "sample": f"{per_step} samples/step x {args.steps} steps, indices from {args.warmup * per_step}"},
+        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
+        "config": config_dict(args, cfg, world),
+        "step": f"one reference sample_block window of {per_step} RRR sets (sampling is ~99% of the reference "
+                "IMM time on these configs, SURVEY.md §3.1; its full IMM re-samples the estimation sets, so "
+                "this rate is an upper bound on the reference's theta / IMM-seconds)",
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def config_dict(args, cfg, world):
+    # identical in both arms (the driver compares them)
+    return {"workload": args.config, "desc": cfg["desc"], "seed": SEED,
+            "l2": "GPU arm: a 256 MB write flushes L2 (126 MB) between steps; the c4 and c5 graphs are also larger than L2",
+            "parallelism": f"replicas x{world}"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -239,7 +296,7 @@ def run_ours(args, cfg, rank, world, local):
     import paper_2208_00613_b200 as im
 
     torch.cuda.set_device(local)
-    dev = im.Device(local)
+    dev = im.default_device(local)
     stream = torch.cuda.ExternalStream(dev.stream, device=f"cuda:{local}")
     transposed = bool(cfg.get("device_gen"))
     if transposed:
@@ -321,7 +378,7 @@ def run_ours(args, cfg, rank, world, local):
     dev.synchronize()
     t0 = time.perf_counter()
     e2e_samples = 0
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = args.steps
     for _ in range(e2e_steps):
         dge = im.DeviceGraph.from_arrays(n, p_off, p_tgt, p_pr, transposed, device=dev)
         if "lt_seed" in cfg:
@@ -367,23 +424,28 @@ def run_ours(args, cfg, rank, world, local):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
-            rate, dt = cpu_reference_rate((off, tgt, pr), n, args.ref_samples, 0, threads, transposed)
-            cpu = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "reference",
-                   "sample": f"reference sample_block, global indices [0, {args.ref_samples}) of the workload, "
-                             f"{dt:.1f} s on {threads} host threads"}
+            per = args.ref_samples or cfg["ref_samples"]
+            rw = ReferenceWindow(cfg)
+            dt = rw.sample(per, 0)
+            cpu = {"value": per / dt, "unit": "samples/s", **rw.describe(per, 1, 0, dt)}
+            del rw
         except Exception as ex:  # reference build missing on this box
             cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32/u64 integer (RNG u64, ids u32)", "data": "synthetic",
-        "config": {"workload": args.config, "desc": cfg["desc"], "l2": "flushed between steps (256 MB write)",
-                   "parallelism": f"replicas x{world}", "theta": r0["theta"], "reuse_pool": True},
+        "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
+        "config": config_dict(args, cfg, world),
+        "theta": r0["theta"], "reuse_pool": True,
         "imm_end_to_end_s": ms / args.steps / 1000.0,
         "compression_ratio": r0["compression_ratio"],
         "dense_sets": r0.get("dense_sets", 0),
         "compression_ratio_device": r0["raw_bytes"] / r0["device_store_bytes"] if r0["device_store_bytes"] else None,
+        "device_memory": {"peak_bytes": r0["device_peak_bytes"], "resident_after_run_bytes": r0["device_resident_bytes"],
+                          "graph_bytes": r0["device_graph_bytes"], "store_bytes": r0["device_store_bytes"],
+                          "ledger_peak_bytes": r0["peak_bytes"],
+                          "note": "peak/resident = stream-ordered pool high-water / in-use bytes of the run (graph "
+                                  "included); ledger = the reference's logical MemoryLedger peak"},
         "edges_examined_per_s": sum(x["edges_scanned"] for x in results) / (ms_local / 1000.0),
         "phase_seconds": r0["phase_seconds"],
         "seeds_head": r0["seeds"][:5],
@@ -413,9 +475,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-samples", type=int, default=20000)
+    ap.add_argument("--ref-samples", type=int, default=0, help="reference window per step (default: per config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

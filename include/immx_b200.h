@@ -212,6 +212,8 @@ IMMX_API int immx_store_info(const immx_store* s, uint64_t* count, uint64_t* pay
  * cp_off[hi-lo+1], copied.  Any pointer may be NULL to skip that array. */
 IMMX_API int immx_store_read(const immx_store* s, uint64_t lo, uint64_t hi, uint64_t* byte_off, uint8_t* bytes,
                     uint64_t* bit_length, uint64_t* cp_off, uint32_t* copied);
+/* the store's codebook (HuffmanCodebook::code_of, huffman.hpp:15-33): n entries each, len 0 = uncoded */
+IMMX_API int immx_store_codebook(const immx_store* s, uint64_t* code_bits, uint8_t* code_len);
 /* huffman.cpp:129-158 decode_find of set j: *found, decoded[] (codable part up to the stop) */
 IMMX_API int immx_store_decode_find(const immx_store* s, uint64_t j, uint32_t top, int* found, uint32_t* decoded,
                            uint64_t* n_decoded);
@@ -251,15 +253,46 @@ typedef struct {
  * (the pipeline always samples on Gt).  Everything stays on the GPU except the
  * scalar control (theta arithmetic, the Huffman tree, characterization). */
 IMMX_API int immx_run(const immx_graph* g, const immx_run_config* cfg, immx_result** out);
-/* scalars: u[0]=theta u[1]=estimation_samples u[2]=exit_iteration u[3]=blocks u[4]=raw_bytes
- *          u[5]=encoded_bytes u[6]=peak_bytes u[7]=padded u[8]=k u[9]=coded_vertices
- *          u[10]=device_store_bytes u[11]=samples_drawn u[12]=edges_scanned u[13]=members
- *          u[14]=dense (bitmap) sets of a HYBRID store
- *          d[0]=covered_fraction d[1]=skewness d[2]=density d[3]=compression_ratio
- *          d[4]=uncoded_vertex_fraction d[5..8]=phase seconds (estimate, sample_encode,
- *          select, total; device-event timed) d[9]=host codebook s d[10]=host decode-table s
- *          i[0]=characterized mode i[1]=mode i[2]=mode_overridden */
-IMMX_API int immx_result_scalars(const immx_result* r, uint64_t* u /*16*/, double* d /*12*/, int* i /*4*/);
+/* The run's statistics (RunStats, pipeline.hpp:45-61, plus device counters).  Versioned:
+ * the caller sets struct_size = sizeof(immx_run_stats) (and may leave version 0); the library
+ * fills min(struct_size, its own size) bytes and writes its version, so a caller built
+ * against an older, shorter layout keeps working when fields are appended. */
+#define IMMX_RUN_STATS_VERSION 1
+typedef struct {
+    uint32_t struct_size;           /* in: sizeof the caller's struct */
+    uint32_t version;               /* out: IMMX_RUN_STATS_VERSION of the library */
+    /* pipeline.hpp RunStats / SamplingPlan */
+    uint64_t theta;
+    uint64_t estimation_samples;
+    uint32_t exit_iteration;        /* 0 = iteration cap */
+    uint32_t blocks;
+    uint32_t k;
+    uint32_t padded;                /* SeedSet::padded */
+    double covered_fraction;        /* F at the final estimation iteration */
+    double skewness, density;       /* characterize.cpp on block 1 */
+    int32_t characterized_mode;     /* IMMX_MODE_* chosen by characterize */
+    int32_t mode;                   /* IMMX_MODE_* used */
+    int32_t mode_overridden;
+    int32_t reserved0;
+    uint64_t raw_bytes, encoded_bytes;   /* sum of block stats (reference formulas) */
+    double compression_ratio;            /* raw_bytes / encoded_bytes (pipeline.cpp:139-146) */
+    uint64_t peak_bytes;                 /* MemoryLedger peak (memory.hpp:9-22), logical */
+    uint64_t coded_vertices;
+    double uncoded_vertex_fraction;
+    double t_estimate, t_sample_encode, t_select, t_total;  /* seconds, phase_seconds */
+    double t_codebook, t_decode_table;   /* host parts of sample_encode (the decode table overlaps) */
+    /* device counters */
+    uint64_t samples_drawn;         /* RRR sets sampled (the estimation sets are reused) */
+    uint64_t edges_scanned;         /* sum of E_j over every sampled set */
+    uint64_t members;               /* sum |R_j| over the theta production sets */
+    uint64_t dense_sets;            /* HYBRID: sets stored as n-bit bitmaps */
+    uint64_t device_store_bytes;    /* the compressed store as held in HBM (side index included) */
+    uint64_t device_peak_bytes;     /* high-water mark of device memory in use during the run
+                                       (stream-ordered pool, graph included) */
+    uint64_t device_resident_bytes; /* device memory in use when the run returned (graph + store) */
+    uint64_t device_graph_bytes;    /* the graph's share of both */
+} immx_run_stats;
+IMMX_API int immx_result_stats(const immx_result* r, immx_run_stats* out);
 IMMX_API int immx_result_seeds(const immx_result* r, uint32_t* seeds, uint64_t* marginal, double* coverage);
 IMMX_API int immx_result_blocks(const immx_result* r, uint64_t* sets, uint64_t* raw_bytes, uint64_t* encoded_bytes);
 /* device objects the run produced (borrowed; NULL when the mode did not create them).  The

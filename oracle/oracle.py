@@ -109,6 +109,40 @@ class Oracle:
         _sig(L, "oc_run_store", None, [P, u64p, u64p, u8p, u64p, u32p])
         _sig(L, "oc_run_codebook", P, [P])
         _sig(L, "oc_run_free", None, [P])
+        _sig(L, "og_rmat", P, [C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64, C.c_int])
+        _sig(L, "og_er", P, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int])
+        _sig(L, "og_csr_n", C.c_uint64, [P])
+        _sig(L, "og_csr_m", C.c_uint64, [P])
+        _sig(L, "og_csr_offsets", C.POINTER(C.c_uint64), [P])
+        _sig(L, "og_csr_targets", C.POINTER(C.c_uint32), [P])
+        _sig(L, "og_csr_free", None, [P])
+        _sig(L, "og_weights_f32", None, [P, C.c_int, C.c_int, C.c_double, f64p])
+        _sig(L, "og_lt_weights", None, [P, C.c_uint64, f32p])
+
+    # ---------------------------------------------------- config graphs (gen_graph.c)
+    def generate(self, gen, weights=("wc", 0.0), reverse: bool = True, lt_seed=None):
+        """A BASELINE-config graph from oracle/gen_graph.c: gen = ("rmat", scale, ef, seed) or
+        ("er", n, m, seed); weights = (model, p) as float32-rounded doubles.  reverse=True gives
+        G^T.  With lt_seed (reverse only) also returns the LT weights (f32 per G^T edge)."""
+        L = self.L
+        h = (L.og_rmat(gen[1], gen[2], 0.57, 0.19, 0.19, gen[3], int(reverse)) if gen[0] == "rmat"
+             else L.og_er(gen[1], gen[2], gen[3], int(reverse)))
+        if not h:
+            raise ValueError("generator arguments out of range")
+        try:
+            n, m = L.og_csr_n(h), L.og_csr_m(h)
+            off = np.ctypeslib.as_array(L.og_csr_offsets(h), shape=(n + 1,)).copy()
+            tgt = np.ctypeslib.as_array(L.og_csr_targets(h), shape=(max(m, 1),))[:m].copy()
+            prob = np.zeros(max(m, 1), np.float64)
+            L.og_weights_f32(h, int(reverse), 0 if weights[0] == "wc" else 1, float(weights[1]), prob)
+            g = CSR(n, off, tgt, prob[:m])
+            if lt_seed is None:
+                return g
+            w = np.zeros(max(m, 1), np.float32)
+            L.og_lt_weights(h, lt_seed, w)
+            return g, w[:m]
+        finally:
+            L.og_csr_free(h)
 
     # ---------------------------------------------------------------- RNG
     def mix64(self, z: int) -> int:
@@ -419,9 +453,29 @@ class RefLib:
         _sig(L, "ref_run_seeds", None, [P, u32p, u64p, f64p, C.POINTER(C.c_uint32)])
         _sig(L, "ref_run_json", C.c_char_p, [P])
         _sig(L, "ref_run_free", None, [P])
+        _sig(L, "ref_graph_generate", P, [C.c_int, C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                          C.c_uint64, C.c_int, C.c_int, C.c_double])
+        _sig(L, "ref_probe_block1", P, [P, C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64])
+        _sig(L, "ref_probe_top", C.c_uint32, [P])
+        _sig(L, "ref_probe_coded", C.c_uint64, [P])
+        _sig(L, "ref_probe_codes", None, [P, u64p, u8p, u64p])
+        _sig(L, "ref_probe_enc_sizes", None, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)])
+        _sig(L, "ref_probe_enc", None, [P, u64p, u8p, u64p, u64p, u32p])
+        _sig(L, "ref_probe_block", P, [P])
+        _sig(L, "ref_probe_free", None, [P])
 
     def graph(self, g: CSR):
         return RefGraph(self, self.L.ref_graph_new(g.n, g.m, g.off, _nz32(g.tgt), _nz64(g.prob)))
+
+    def generate(self, gen, weights=("wc", 0.0), reverse: bool = False):
+        """A BASELINE-config graph built inside the reference library by oracle/gen_graph.c
+        (no Python copy: the c5 graph is 17 GB as immx::Graph).  reverse=False: forward."""
+        kind = 0 if gen[0] == "rmat" else 1
+        h = self.L.ref_graph_generate(kind, gen[1], gen[2], 0.57, 0.19, 0.19, gen[3], int(reverse),
+                                      0 if weights[0] == "wc" else 1, float(weights[1]))
+        if not h:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        return RefGraph(self, h)
 
     def load(self, path: str):
         h = self.L.ref_graph_load(path.encode())
@@ -464,6 +518,42 @@ class RefGraph:
         L.ref_block_copy(b, offs, mem)
         L.ref_block_free(b)
         return offs, mem[:tot].copy()
+
+    def probe_block1(self, per_block, seed, workers, lo, hi):
+        """Block 1 of run() through the reference's public functions (ref_shim.cpp
+        ref_probe_block1): codebook, block-1 histogram, top, raw and encoded sets [lo, hi)."""
+        L = self.r.L
+        h = L.ref_probe_block1(self.h, per_block, seed, workers, lo, hi)
+        if not h:
+            raise RuntimeError(L.ref_last_error().decode())
+        try:
+            n = self.n
+            bits = np.zeros(n, np.uint64)
+            lens = np.zeros(n, np.uint8)
+            hist = np.zeros(n, np.uint64)
+            L.ref_probe_codes(h, bits, lens, hist)
+            nb, nc = C.c_uint64(), C.c_uint64()
+            L.ref_probe_enc_sizes(h, C.byref(nb), C.byref(nc))
+            w = hi - lo
+            byte_off = np.zeros(w + 1, np.uint64)
+            data = np.zeros(max(nb.value, 1), np.uint8)
+            bitlen = np.zeros(max(w, 1), np.uint64)
+            cp_off = np.zeros(w + 1, np.uint64)
+            copied = np.zeros(max(nc.value, 1), np.uint32)
+            L.ref_probe_enc(h, byte_off, data, bitlen, cp_off, copied)
+            b = L.ref_probe_block(h)
+            tot = L.ref_block_total(b)
+            offs = np.zeros(per_block + 1, np.uint64)
+            mem = np.zeros(max(tot, 1), np.uint32)
+            L.ref_block_copy(b, offs, mem)
+            raw_off = offs[lo:hi + 1] - offs[lo]
+            raw = mem[int(offs[lo]):int(offs[hi])].copy()
+            return {"top": int(L.ref_probe_top(h)), "coded": int(L.ref_probe_coded(h)), "code_bits": bits,
+                    "code_len": lens, "hist": hist, "enc_byte_off": byte_off, "enc_bytes": data[:nb.value],
+                    "enc_bitlen": bitlen[:w], "enc_cp_off": cp_off, "enc_copied": copied[:nc.value],
+                    "raw_off": raw_off, "raw": raw, "block_members": int(tot)}
+        finally:
+            L.ref_probe_free(h)
 
     def estimate_theta(self, k, eps, seed=42, workers=1):
         out = np.zeros(3, np.uint64)

@@ -86,10 +86,13 @@ class Device:
 _DEFAULT = None
 
 
-def default_device() -> Device:
+def default_device(ordinal: int | None = None) -> Device:
+    """The process's immx_device (the C-ABI admits one live context per process)."""
     global _DEFAULT
     if _DEFAULT is None:
-        _DEFAULT = Device(0)
+        _DEFAULT = Device(0 if ordinal is None else ordinal)
+    elif ordinal is not None and ordinal != _DEFAULT.ordinal:
+        raise ValueError(f"the process already uses cuda:{_DEFAULT.ordinal} (one immx_device per process)")
     return _DEFAULT
 
 
@@ -506,6 +509,12 @@ class Store:
         check(lib.immx_store_info(self.h, C.byref(c), C.byref(p), C.byref(d)))
         return {"count": c.value, "payload_bytes": p.value, "device_bytes": d.value}
 
+    def codebook(self, n: int):
+        """(code_bits u64[n], code_len u8[n]) of the store's codebook (len 0: uncoded, bits 0)."""
+        bits, lens = np.zeros(n, np.uint64), np.zeros(n, np.uint8)
+        check(lib.immx_store_codebook(self.h, ptr(bits, C.c_uint64), ptr(lens, C.c_uint8)))
+        return bits, lens
+
     def read(self, lo: int, hi: int):
         cnt = hi - lo
         bo = np.zeros(cnt + 1, np.uint64)
@@ -667,9 +676,20 @@ def _sel_dict(seeds, marg, cov, padded):
     return {"seeds": seeds.tolist(), "marginal": marg.tolist(), "coverage": cov.tolist(), "padded": padded.value}
 
 
+def _check_merged(merged: bool, workers: int) -> None:
+    """select.cpp:71-74: with merged_argmax and more than one worker the reference picks from
+    the per-chunk winners only (a heuristic, not the exact argmax).  That mode is out of scope
+    here, so it is refused rather than silently answered exactly; with one
+    worker the reference itself falls back to the exact argmax, and so does this."""
+    if merged and workers > 1:
+        raise ValueError("merged_argmax with workers > 1 (the reference's per-chunk heuristic pick) is not "
+                         "supported by the B200 path, which selects with the exact argmax")
+
+
 def select_raw(sets, n: int, k: int, workers: int = 1, merged_argmax: bool = False):
-    """select.cpp:89-148 (exact argmax; merged_argmax is the reference's non-exact multi-worker
-    heuristic, SURVEY §2 marks it out of scope, so the selection stays exact)."""
+    """select.cpp:89-148 with the exact argmax (ties -> lowest id).  merged_argmax=True with
+    workers > 1 raises ValueError (see _check_merged)."""
+    _check_merged(merged_argmax, workers)
     if len(sets) == 0:
         raise ValueError("selection requires at least one set")
     pool = Pool()
@@ -728,28 +748,32 @@ def run_device(dg: DeviceGraph, k: int, *, epsilon=0.5, blocks=8, mode="auto", s
     h = C.c_void_p()
     check(lib.immx_run(dg.h, C.byref(cfg), C.byref(h)))
     try:
-        u = np.zeros(16, np.uint64)
-        d = np.zeros(12, np.float64)
-        i = np.zeros(4, np.int32)
-        check(lib.immx_result_scalars(h, ptr(u, C.c_uint64), ptr(d, C.c_double), ptr(i, C.c_int)))
+        st = _capi.immx_run_stats()
+        st.struct_size = C.sizeof(st)
+        check(lib.immx_result_stats(h, C.byref(st)))
+        if st.version != _capi.RUN_STATS_VERSION:
+            raise RuntimeError(f"immx_run_stats version {st.version}, expected {_capi.RUN_STATS_VERSION}")
         seeds, marg, cov = np.zeros(k, np.uint32), np.zeros(k, np.uint64), np.zeros(k, np.float64)
         check(lib.immx_result_seeds(h, ptr(seeds, C.c_uint32), ptr(marg, C.c_uint64), ptr(cov, C.c_double)))
-        b = int(u[3])
+        b = int(st.blocks)
         bs, br, be = np.zeros(b, np.uint64), np.zeros(b, np.uint64), np.zeros(b, np.uint64)
         check(lib.immx_result_blocks(h, ptr(bs, C.c_uint64), ptr(br, C.c_uint64), ptr(be, C.c_uint64)))
         out = {
-            "seeds": seeds.tolist(), "marginal": marg.tolist(), "coverage": cov.tolist(), "padded": int(u[7]),
-            "theta": int(u[0]), "estimation_samples": int(u[1]), "exit_iteration": int(u[2]), "blocks": b,
-            "raw_bytes": int(u[4]), "encoded_bytes": int(u[5]), "peak_bytes": int(u[6]),
-            "coded_vertices": int(u[9]), "device_store_bytes": int(u[10]), "samples_drawn": int(u[11]),
-            "edges_scanned": int(u[12]), "pool_members": int(u[13]), "dense_sets": int(u[14]),
-            "covered_fraction": float(d[0]), "skewness": float(d[1]), "density": float(d[2]),
-            "compression_ratio": float(d[3]), "uncoded_vertex_fraction": float(d[4]),
-            "phase_seconds": {"estimate": float(d[5]), "sample_encode": float(d[6]), "select": float(d[7]),
-                              "total": float(d[8])},
-            "host_seconds": {"codebook": float(d[9]), "decode_table": float(d[10])},
-            "characterized_mode": _MODE_NAME[int(i[0])], "mode": _MODE_NAME[int(i[1])],
-            "mode_override": bool(i[2]),
+            "seeds": seeds.tolist(), "marginal": marg.tolist(), "coverage": cov.tolist(), "padded": st.padded,
+            "theta": st.theta, "estimation_samples": st.estimation_samples, "exit_iteration": st.exit_iteration,
+            "blocks": b, "raw_bytes": st.raw_bytes, "encoded_bytes": st.encoded_bytes, "peak_bytes": st.peak_bytes,
+            "coded_vertices": st.coded_vertices, "device_store_bytes": st.device_store_bytes,
+            "samples_drawn": st.samples_drawn, "edges_scanned": st.edges_scanned, "pool_members": st.members,
+            "dense_sets": st.dense_sets, "covered_fraction": st.covered_fraction, "skewness": st.skewness,
+            "density": st.density, "compression_ratio": st.compression_ratio,
+            "uncoded_vertex_fraction": st.uncoded_vertex_fraction,
+            "phase_seconds": {"estimate": st.t_estimate, "sample_encode": st.t_sample_encode, "select": st.t_select,
+                              "total": st.t_total},
+            "host_seconds": {"codebook": st.t_codebook, "decode_table": st.t_decode_table},
+            "characterized_mode": _MODE_NAME[st.characterized_mode], "mode": _MODE_NAME[st.mode],
+            "mode_override": bool(st.mode_overridden),
+            "device_peak_bytes": st.device_peak_bytes, "device_resident_bytes": st.device_resident_bytes,
+            "device_graph_bytes": st.device_graph_bytes,
             "block_sets": bs.tolist(), "block_raw": br.tolist(), "block_enc": be.tolist(),
         }
         if keep:
@@ -778,6 +802,7 @@ def run(graph: Graph, k: int, *, epsilon=0.5, blocks=8, mode="auto", seed=42, wo
         raise ValueError(f"unknown mode '{mode}'")
     if diffusion not in ("ic", "lt"):
         raise ValueError(f"unknown diffusion model '{diffusion}'")
+    _check_merged(merged_argmax, workers)
     dg = DeviceGraph(graph, transposed=False)
     model = _capi.MODEL_IC
     if diffusion == "lt":

@@ -51,6 +51,23 @@ class immx_run_config(C.Structure):
                 ("workers", C.c_int), ("model", C.c_int), ("reuse_pool", C.c_int)]
 
 
+class immx_run_stats(C.Structure):
+    """include/immx_b200.h immx_run_stats (IMMX_RUN_STATS_VERSION 1), field for field."""
+    _fields_ = [("struct_size", u32), ("version", u32),
+                ("theta", u64), ("estimation_samples", u64), ("exit_iteration", u32), ("blocks", u32),
+                ("k", u32), ("padded", u32), ("covered_fraction", dbl), ("skewness", dbl), ("density", dbl),
+                ("characterized_mode", C.c_int32), ("mode", C.c_int32), ("mode_overridden", C.c_int32),
+                ("reserved0", C.c_int32), ("raw_bytes", u64), ("encoded_bytes", u64), ("compression_ratio", dbl),
+                ("peak_bytes", u64), ("coded_vertices", u64), ("uncoded_vertex_fraction", dbl),
+                ("t_estimate", dbl), ("t_sample_encode", dbl), ("t_select", dbl), ("t_total", dbl),
+                ("t_codebook", dbl), ("t_decode_table", dbl),
+                ("samples_drawn", u64), ("edges_scanned", u64), ("members", u64), ("dense_sets", u64),
+                ("device_store_bytes", u64), ("device_peak_bytes", u64), ("device_resident_bytes", u64),
+                ("device_graph_bytes", u64)]
+
+
+RUN_STATS_VERSION = 1
+
 I = C.c_int
 # name: (restype, argtypes) -- exactly include/immx_b200.h
 SIGNATURES = {
@@ -110,6 +127,7 @@ SIGNATURES = {
     "immx_store_info": (I, [P, pu64, pu64, pu64]),
     "immx_store_set_hybrid": (I, [P, C.c_int]),
     "immx_store_read": (I, [P, u64, u64, pu64, pu8, pu64, pu64, pu32]),
+    "immx_store_codebook": (I, [P, pu64, pu8]),
     "immx_store_decode_find": (I, [P, u64, u32, pint, pu32, pu64]),
     "immx_select_huffman": (I, [P, pu64, u32, pu32, pu64, pdbl, pu32, pu64]),
     "immx_bitmap_create": (I, [P, u64, PP]),
@@ -121,7 +139,7 @@ SIGNATURES = {
     "immx_bitmap_subtract_row": (I, [P, u32, pu32, pu64]),
     "immx_select_bitmap": (I, [P, pu64, u32, pu32, pu64, pdbl, pu32]),
     "immx_run": (I, [P, C.POINTER(immx_run_config), PP]),
-    "immx_result_scalars": (I, [P, pu64, pdbl, pint]),
+    "immx_result_stats": (I, [P, C.POINTER(immx_run_stats)]),
     "immx_result_seeds": (I, [P, pu32, pu64, pdbl]),
     "immx_result_blocks": (I, [P, pu64, pu64, pu64]),
     "immx_result_pool": (P, [P]),

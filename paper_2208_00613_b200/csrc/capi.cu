@@ -7,6 +7,7 @@
 // scalar control (theta arithmetic sampler.cpp:54-83, characterization characterize.cpp,
 // the Huffman tree huffman.cpp:24-84, the memory ledger memory.hpp) on the host.
 #include <cub/cub.cuh>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 
@@ -164,9 +165,7 @@ uint64_t pool_members_range(const Pool& P, uint64_t lo, uint64_t hi) {
 
 // ---- the run result -----------------------------------------------------------------
 struct immx_result {
-    uint64_t u[16] = {0};
-    double dd[12] = {0};
-    int ii[4] = {0};
+    immx_run_stats st{};
     std::vector<uint32_t> seeds;
     std::vector<uint64_t> marginal;
     std::vector<double> coverage;
@@ -343,6 +342,18 @@ int immx_device_create(int ordinal, immx_device** out) {
         if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
             fail(IMMX_ECUDA, "no CUDA device is available (the B200 path has no CPU fallback)");
         if (ordinal < 0 || ordinal >= count) fail(IMMX_EINVAL, "device ordinal out of range");
+        // every device allocation is ordered on the one allocation stream (internal.hpp
+        // alloc_stream), which is this context's work stream: a second live context would
+        // re-point it and leave the first one's frees unordered with its kernels
+        int expected = 0;
+        if (!live_devices().compare_exchange_strong(expected, 1))
+            fail(IMMX_ERUNTIME, "one immx_device per process: destroy the existing device first");
+        struct Admit {  // a failure below releases the slot again
+            bool ok = false;
+            ~Admit() {
+                if (!ok) live_devices().store(0);
+            }
+        } admit;
         CK(cudaSetDevice(ordinal));
         auto* h = new immx_device;
         Device& d = h->d;
@@ -357,6 +368,7 @@ int immx_device_create(int ordinal, immx_device** out) {
         CK(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep_all));
         d.scal.exact(64);
         CK(cudaMallocHost(&d.host_scal, 64 * 8));
+        admit.ok = true;
         *out = h;
     });
 }
@@ -374,6 +386,7 @@ void immx_device_destroy(immx_device* h) {
     cudaStreamSynchronize(h->d.stream);
     cudaStreamDestroy(h->d.stream);
     delete h;
+    live_devices().store(0);
 }
 void* immx_device_stream(immx_device* h) { return h ? (void*)h->d.stream : nullptr; }
 int immx_device_synchronize(immx_device* h) {
@@ -716,6 +729,22 @@ int immx_store_read(const immx_store* s, uint64_t lo, uint64_t hi, uint64_t* byt
         store_read_host(s->s, lo, hi, byte_off, bytes, bit_length, cp_off, copied);
     });
 }
+int immx_store_codebook(const immx_store* s, uint64_t* code_bits, uint8_t* code_len) {
+    return guard([&] {
+        need(s, "store");
+        const Store& S = s->s;
+        if (!S.dev || !S.n) fail(IMMX_ERUNTIME, "the store has no codebook");
+        cudaStream_t st = S.dev->stream;
+        std::vector<uint8_t> len(S.n);
+        CK(cudaMemcpyAsync(len.data(), S.code_len.p, S.n, cudaMemcpyDeviceToHost, st));
+        if (code_bits) CK(cudaMemcpyAsync(code_bits, S.code_bits.p, S.n * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (code_len) std::memcpy(code_len, len.data(), S.n);
+        if (code_bits)  // uncoded vertices read back as bits 0 (HuffmanCodebook::Code{})
+            for (uint64_t v = 0; v < S.n; ++v)
+                if (!len[v]) code_bits[v] = 0;
+    });
+}
 int immx_store_decode_find(const immx_store* s, uint64_t j, uint32_t top, int* found, uint32_t* decoded,
                            uint64_t* n_decoded) {
     return guard([&] {
@@ -846,6 +875,8 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
 
         auto* R = new immx_result;
         std::unique_ptr<immx_result> guard_r(R);
+        CK(cudaStreamSynchronize(st));
+        mempool_reset_high(d.ordinal);  // device_peak_bytes = this run's high-water mark
         // the device keeps the run's pool (its multi-GB arena) for the next run; the result
         // borrows it (valid until the next immx_run on this device)
         if (!d.run_pool) {
@@ -863,6 +894,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         const double t_est = secs(t0);
         uint64_t samples_drawn = pool.count;
         const uint64_t theta = plan.theta;
+        if (theta >= 0xffffffffULL) fail(IMMX_EINVAL, "theta above 2^32-1 sets");
         const uint32_t b = (uint32_t)std::min<uint64_t>(cfg->blocks, std::max<uint64_t>(theta, 1));
         const uint64_t per_block = (theta + b - 1) / b;
 
@@ -871,20 +903,21 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         auto ckpt = [&] { peak = std::max(peak, led_raw + led_enc + led_freq + led_dec); };
 
         t0 = Clock::now();
-        if (cfg->reuse_pool) {
-            // sets [0, estimation_samples) already exist and are bit-identical to what the
-            // production loop would re-draw (same (seed, index) streams)
-            if (theta > pool.count) {
-                sample_into_pool(pool, G, theta - pool.count, pool.count, cfg->rng_seed, nullptr, nullptr, cfg->model);
-                samples_drawn += theta - plan.estimation_samples;
-            }
-        } else {
-            pool_reset(pool);
+        // Raw sets are held block by block (pipeline.cpp:84-133): the pool holds global indices
+        // [pool_base, pool_base + pool.count).  With reuse_pool the estimation sets [0, E) are
+        // the first production sets (same (seed, index) streams, sampler.hpp:64-66), so the
+        // blocks inside [0, E) are encoded from them; every later block is sampled into an
+        // emptied pool, encoded, and its memory released -- except in raw mode, where the sets
+        // are the store (the reference keeps raw_blocks too, pipeline.cpp:124-127).
+        uint64_t pool_base = 0, edges_released = 0;
+        if (!cfg->reuse_pool) {
+            edges_released += pool.edges;
+            pool_release(pool);
         }
         int mode = IMMX_MODE_RAW, char_mode = IMMX_MODE_RAW;
         double t_codebook = 0.0, t_lut = 0.0;  // host: Huffman tree, decode table
-        std::future<void> lut_job;             // the decode table, built beside the encode
-        uint32_t lut_rb = 1;
+        uint32_t lut_rb = 1;                   // (declared before lut_job: the job writes them and
+        std::future<void> lut_job;             //  the future's destructor joins it on unwinding)
         double skew = 0.0, dens = 0.0;
         if (!d.run_cb) d.run_cb = std::make_shared<HostCodebook>();
         HostCodebook& cb = *d.run_cb;
@@ -897,11 +930,18 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         uint64_t done = 0;
         for (uint32_t i = 1; i <= b; ++i) {
             const uint64_t count = std::min(per_block, theta - done);
-            const uint64_t lo = done, hi = done + count;
-            if (!cfg->reuse_pool) {
-                sample_into_pool(pool, G, count, done, cfg->rng_seed, nullptr, nullptr, cfg->model);
-                samples_drawn += count;
+            const uint64_t glo = done, ghi = done + count;  // global indices of block i
+            if (pool_base + pool.count < ghi) {
+                if (i > 1 && mode != IMMX_MODE_RAW && glo >= pool_base + pool.count) {
+                    edges_released += pool.edges;  // the previous block's sets are encoded
+                    pool_release(pool);
+                    pool_base = glo;
+                }
+                const uint64_t from = pool_base + pool.count;
+                sample_into_pool(pool, G, ghi - from, from, cfg->rng_seed, nullptr, nullptr, cfg->model);
+                samples_drawn += ghi - from;
             }
+            const uint64_t lo = glo - pool_base, hi = ghi - pool_base;  // pool-relative
             done += count;
             const uint64_t raw = 4 * pool_members_range(pool, lo, hi);
             led_raw += raw;
@@ -914,6 +954,10 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                 dens = density_host(sizes.data(), count, n);
                 char_mode = choose_encoding_host(skew, dens);
                 mode = cfg->mode >= 0 ? cfg->mode : char_mode;
+                if (mode != IMMX_MODE_RAW) {  // the estimation's inverted index and running table
+                    pool.rix.reset();
+                    d.ws_hist.release();
+                }
                 if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {
                     // block 1's table is also the encode-time table after block 1 (counted once)
                     pool_hist_dev(pool, lo, hi, hist.p);
@@ -966,7 +1010,14 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                 enc = raw;
             }
             ckpt();
-            if (mode != IMMX_MODE_RAW) led_raw -= raw;
+            if (mode != IMMX_MODE_RAW) {
+                led_raw -= raw;
+                if (hi >= pool.count) {  // every pooled set is encoded: release the raw sets
+                    edges_released += pool.edges;
+                    pool_release(pool);
+                    pool_base = ghi;
+                }
+            }
             ckpt();
             R->blk_sets.push_back(count);
             R->blk_raw.push_back(raw);
@@ -1026,35 +1077,44 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         } else {
             store_dev_bytes = pool.members * 4 + pool.count * 12;
         }
-        R->u[0] = theta;
-        R->u[1] = plan.estimation_samples;
-        R->u[2] = plan.exit_iteration;
-        R->u[3] = b;
-        R->u[4] = raw_total;
-        R->u[5] = enc_total;
-        R->u[6] = peak;
-        R->u[7] = sel.padded;
-        R->u[8] = k;
-        R->u[9] = cb.coded;
-        R->u[10] = store_dev_bytes;
-        R->u[11] = samples_drawn;
-        R->u[12] = pool.edges;
-        R->u[13] = pool.members;
-        R->u[14] = store ? store->s.dense_count : 0;
-        R->dd[0] = plan.covered_fraction;
-        R->dd[1] = skew;
-        R->dd[2] = dens;
-        R->dd[3] = ratio;
-        R->dd[4] = uncoded;
-        R->dd[5] = t_est;
-        R->dd[6] = t_samp;
-        R->dd[7] = t_sel;
-        R->dd[8] = t_total;
-        R->dd[9] = t_codebook;
-        R->dd[10] = t_lut;
-        R->ii[0] = char_mode;
-        R->ii[1] = mode;
-        R->ii[2] = cfg->mode >= 0 && cfg->mode != char_mode;
+        hist.release();
+        device_trim(d);
+        CK(cudaStreamSynchronize(st));
+        immx_run_stats& o = R->st;
+        o.struct_size = sizeof(immx_run_stats);
+        o.version = IMMX_RUN_STATS_VERSION;
+        o.theta = theta;
+        o.estimation_samples = plan.estimation_samples;
+        o.exit_iteration = plan.exit_iteration;
+        o.blocks = b;
+        o.k = k;
+        o.padded = sel.padded;
+        o.covered_fraction = plan.covered_fraction;
+        o.skewness = skew;
+        o.density = dens;
+        o.characterized_mode = char_mode;
+        o.mode = mode;
+        o.mode_overridden = cfg->mode >= 0 && cfg->mode != char_mode;
+        o.raw_bytes = raw_total;
+        o.encoded_bytes = enc_total;
+        o.compression_ratio = ratio;
+        o.peak_bytes = peak;
+        o.coded_vertices = cb.coded;
+        o.uncoded_vertex_fraction = uncoded;
+        o.t_estimate = t_est;
+        o.t_sample_encode = t_samp;
+        o.t_select = t_sel;
+        o.t_total = t_total;
+        o.t_codebook = t_codebook;
+        o.t_decode_table = t_lut;
+        o.samples_drawn = samples_drawn;
+        o.edges_scanned = edges_released + pool.edges;
+        o.members = raw_total / 4;
+        o.dense_sets = store ? store->s.dense_count : 0;
+        o.device_store_bytes = store_dev_bytes;
+        o.device_peak_bytes = mempool_attr(d.ordinal, cudaMemPoolAttrUsedMemHigh);
+        o.device_resident_bytes = mempool_attr(d.ordinal, cudaMemPoolAttrUsedMemCurrent);
+        o.device_graph_bytes = G.device_bytes();
         R->seeds = sel.seeds;
         R->marginal = sel.marginal;
         R->coverage = sel.coverage;
@@ -1063,12 +1123,17 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
     });
 }
 
-int immx_result_scalars(const immx_result* r, uint64_t* u, double* dd, int* ii) {
+int immx_result_stats(const immx_result* r, immx_run_stats* out) {
     return guard([&] {
         need(r, "result");
-        if (u) std::memcpy(u, r->u, sizeof(r->u));
-        if (dd) std::memcpy(dd, r->dd, sizeof(r->dd));
-        if (ii) std::memcpy(ii, r->ii, sizeof(r->ii));
+        need(out, "out");
+        if (out->struct_size < offsetof(immx_run_stats, theta))
+            fail(IMMX_EINVAL, "immx_run_stats.struct_size must be set to sizeof(immx_run_stats)");
+        const uint32_t want = out->struct_size;
+        const size_t nb = std::min<size_t>(want, sizeof(immx_run_stats));
+        std::memcpy(out, &r->st, nb);
+        out->struct_size = want;
+        out->version = IMMX_RUN_STATS_VERSION;
     });
 }
 int immx_result_seeds(const immx_result* r, uint32_t* seeds, uint64_t* marg, double* cov) {

@@ -39,6 +39,10 @@ inline cudaStream_t& alloc_stream() {
     static cudaStream_t s = nullptr;
     return s;
 }
+inline std::atomic<int>& live_devices() {  // immx_device_create admits one live context
+    static std::atomic<int> n{0};
+    return n;
+}
 inline bool& async_alloc() {  // IMMX_SYNC_ALLOC=1 selects plain cudaMalloc/cudaFree
     static bool a = true;
     return a;
@@ -134,6 +138,36 @@ struct Device {
     double seen_mean = 0.0;
 };
 
+// grow-only workspaces back to the allocator (end of immx_run: only the graph and the store
+// stay in use; the stream-ordered pool keeps the pages reserved, so the next run re-acquires
+// them without a cudaMalloc)
+inline void device_trim(Device& d) {
+    for (auto* b : {&d.ws_list[0], &d.ws_list[1], &d.ws_nospace, &d.ws_qscratch, &d.ws_gbits, &d.ws_pbits, &d.ws_pq,
+                    &d.ws_pbusy, &d.ws_idx})
+        b->release();
+    d.ws_hist.release();
+    d.ws_ctl.release();
+    d.ws_idx_off.release();
+    d.ws_cnt64.release();
+    d.ws_cursor.release();
+    d.ws_covered.release();
+    d.ws_is_seed.release();
+    d.tmp.release();
+}
+// device memory in use from the stream-ordered pool (all immx allocations go through it)
+inline uint64_t mempool_attr(int ordinal, cudaMemPoolAttr a) {
+    cudaMemPool_t mp;
+    uint64_t v = 0;
+    if (cudaDeviceGetDefaultMemPool(&mp, ordinal) == cudaSuccess) cudaMemPoolGetAttribute(mp, a, &v);
+    return v;
+}
+inline void mempool_reset_high(int ordinal) {
+    cudaMemPool_t mp;
+    uint64_t z = 0;
+    if (cudaDeviceGetDefaultMemPool(&mp, ordinal) == cudaSuccess)
+        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrUsedMemHigh, &z);
+}
+
 inline uint64_t next_graph_uid() {  // identity of a device graph (sampler caches key on it)
     static std::atomic<uint64_t> c{0};
     return ++c;
@@ -153,6 +187,9 @@ struct DevGraph {
     bool has_lt = false;
     bool row_dups = false;  // some Gt row holds a repeated target
     uint32_t max_deg = 0;
+    uint64_t device_bytes() const {
+        return row.cap * 8 + col.cap * 4 + thr.cap * 8 + thr_fill.cap * 8 + lt_cum.cap * 8;
+    }
 };
 
 // Raw RRR pool: sets live in an arena (bump-allocated chunks); set j of the pool is
@@ -188,6 +225,15 @@ struct Pool {
 inline void pool_reset(Pool& P) {
     P.count = P.members = P.edges = P.arena_used = 0;
     ++P.epoch;
+}
+// empty the pool AND return its memory (arena, per-set arrays, select_raw's index) to the
+// stream-ordered allocator: immx_run drops each raw block once it is encoded (pipeline.cpp:129-133)
+inline void pool_release(Pool& P) {
+    pool_reset(P);
+    P.arena.release();
+    P.off.release();
+    P.len.release();
+    P.rix.reset();
 }
 
 // Huffman-encoded store.  Set j: words[woff[j] ..] holds its MSB-first byte stream

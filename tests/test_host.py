@@ -188,3 +188,14 @@ def test_lt_weights_normalised(im):
         if off[v + 1] > off[v]:
             assert abs(float(w[off[v]:off[v + 1]].astype(np.float64).sum()) - 1.0) < 1e-5
     assert np.all(w > 0)
+
+
+def test_merged_argmax_multiworker_refused(im):
+    """select.cpp:71-74: merged_argmax with > 1 worker is the reference's per-chunk heuristic;
+    the device path selects exactly, so the flag is refused instead of silently ignored."""
+    g = im.generate_er(50, 300, 1)
+    im.assign_weights_f32(g, "wc")
+    with pytest.raises(ValueError, match="merged_argmax"):
+        im.run(g, 3, merged_argmax=True, workers=4)
+    with pytest.raises(ValueError, match="merged_argmax"):
+        im.select_raw([[0, 1], [2]], 5, 1, workers=2, merged_argmax=True)
