@@ -182,17 +182,26 @@ def test_c5_sample_window_equals_oracle(im, orc):
     assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
 
 
-def test_run_releases_raw_sets_and_reports_device_memory(im):
+def test_run_releases_raw_sets_and_reports_device_memory():
     """pipeline.cpp:129-133: raw blocks are dropped once encoded.  After a Huffman run only the
-    graph and the compressed store stay in use; the high-water mark is reported."""
-    dg = im.DeviceGraph.generate_rmat(16, 16, 0.57, 0.19, 0.19, 5, weights="wc")
-    r = im.run_device(dg, 20, epsilon=0.5, blocks=8, mode="huffman", seed=42)
-    assert r["device_graph_bytes"] > 0 and r["device_store_bytes"] > 0
-    assert r["device_peak_bytes"] >= r["device_resident_bytes"] > 0
-    # resident = graph + store (+ small per-device scalars and the store's decode table / codes)
-    slack = 64 * 1024 * 1024
-    assert r["device_resident_bytes"] <= r["device_graph_bytes"] + 2 * r["device_store_bytes"] + slack
-    assert r["device_peak_bytes"] > r["device_resident_bytes"]
+    graph and the compressed store stay in use; the high-water mark is reported.  (A fresh
+    process: the in-use figure is process-wide.)"""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "mem_probe.py"), "16"], capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    runs = [eval(line.split(" ", 1)[1]) for line in out.stdout.strip().splitlines()]
+    for r in runs:
+        assert r["device_graph_bytes"] > 0 and r["device_store_bytes"] > 0
+        assert r["device_peak_bytes"] > r["device_resident_bytes"] > 0
+        # resident = graph + store (+ the store's codes / decode table and per-device scalars)
+        assert r["device_resident_bytes"] <= r["device_graph_bytes"] + 2 * r["device_store_bytes"] + (16 << 20)
+    # repeated runs neither leak nor grow
+    assert runs[2]["device_resident_bytes"] == runs[1]["device_resident_bytes"]
 
 
 def test_second_device_context_refused(im):
