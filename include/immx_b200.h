@@ -160,9 +160,12 @@ IMMX_API int immx_pool_clear(immx_pool* p);
 IMMX_API int immx_pool_sample(immx_pool* p, const immx_graph* g, uint64_t count, uint64_t first_index,
                      uint64_t seed, int model);
 /* sampler.cpp:14-45 sample_rrr with explicit roots and raw Rng states (module.cpp:110-116:
- * Python sample_rrr uses Rng(seed), i.e. state = seed, coins from the first draw). */
+ * Python sample_rrr uses Rng(seed), i.e. state = seed, coins from the first draw).  The Rng
+ * with state s yields draw t = mix64(s + t*gamma), t = 1, 2, ...; next_draw (may be NULL)
+ * receives per sample the t of the first unused draw, so the caller's Rng advances to
+ * state s + (next_draw - 1)*gamma exactly as the reference's sample_rrr(g_t, root, rng) leaves it. */
 IMMX_API int immx_pool_sample_rooted(immx_pool* p, const immx_graph* g, const uint32_t* roots,
-                            const uint64_t* states, uint64_t count, int model);
+                            const uint64_t* states, uint64_t count, int model, uint64_t* next_draw);
 /* append host sets (CSR) -- for the set-level API (select_raw(sets), build_codebook(sets)) */
 IMMX_API int immx_pool_upload(immx_pool* p, const uint64_t* offsets, const uint32_t* members, uint64_t count);
 IMMX_API int immx_pool_info(const immx_pool* p, uint64_t* count, uint64_t* members, uint64_t* edges_scanned);

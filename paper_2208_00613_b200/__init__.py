@@ -325,8 +325,13 @@ class Pool:
         check(lib.immx_pool_sample(self.h, dg.h, count, first, seed, model))
 
     def sample_rooted(self, dg: DeviceGraph, roots, states, model: int = _capi.MODEL_IC):
+        """Samples from explicit roots and raw Rng states; returns per sample the index of the
+        next unused draw of its stream (draws consumed = next_draw - 1)."""
         r, s = arr(roots, np.uint32), arr(states, np.uint64)
-        check(lib.immx_pool_sample_rooted(self.h, dg.h, ptr(r, C.c_uint32), ptr(s, C.c_uint64), r.size, model))
+        nd = np.zeros(max(r.size, 1), np.uint64)
+        check(lib.immx_pool_sample_rooted(self.h, dg.h, ptr(r, C.c_uint32), ptr(s, C.c_uint64), r.size, model,
+                                          ptr(nd, C.c_uint64)))
+        return nd[: r.size]
 
     def upload(self, sets):
         off, mem = _sets_csr(sets)

@@ -112,7 +112,7 @@ SIGNATURES = {
     "immx_pool_destroy": (None, [P]),
     "immx_pool_clear": (I, [P]),
     "immx_pool_sample": (I, [P, P, u64, u64, u64, I]),
-    "immx_pool_sample_rooted": (I, [P, P, pu32, pu64, u64, I]),
+    "immx_pool_sample_rooted": (I, [P, P, pu32, pu64, u64, I, pu64]),
     "immx_pool_upload": (I, [P, pu64, pu32, u64]),
     "immx_pool_info": (I, [P, pu64, pu64, pu64]),
     "immx_pool_read": (I, [P, u64, u64, pu64, pu32]),

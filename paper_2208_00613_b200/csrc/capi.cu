@@ -25,7 +25,8 @@
 
 
 namespace immx_dev {
-immx_hgraph* load_edge_list(std::istream& in, bool directed);
+immx_hgraph* load_edge_list(const char* data, size_t len, bool directed);
+immx_hgraph* load_edge_list_file(const std::string& path, bool directed);
 immx_hgraph* transpose_host(const immx_hgraph& g);
 void assign_weights_host(immx_hgraph& g, int model, double p, bool f32);
 void save_cache(const immx_hgraph& g, const std::string& path);
@@ -185,16 +186,13 @@ int immx_hgraph_load_edge_list(const char* path, int directed, immx_hgraph** out
     return guard([&] {
         need(path, "path");
         need(out, "out");
-        std::ifstream in(path);
-        if (!in) fail(IMMX_ERUNTIME, std::string("cannot open '") + path + "'");
-        *out = load_edge_list(in, directed != 0);
+        *out = load_edge_list_file(path, directed != 0);
     });
 }
 int immx_hgraph_load_edge_text(const char* text, size_t len, int directed, immx_hgraph** out) {
     return guard([&] {
         need(out, "out");
-        std::istringstream in(std::string(text ? text : "", text ? len : 0));
-        *out = load_edge_list(in, directed != 0);
+        *out = load_edge_list(text ? text : "", text ? len : 0, directed != 0);
     });
 }
 int immx_hgraph_load_cache(const char* path, immx_hgraph** out) {
@@ -509,7 +507,7 @@ int immx_pool_sample(immx_pool* p, const immx_graph* g, uint64_t count, uint64_t
     });
 }
 int immx_pool_sample_rooted(immx_pool* p, const immx_graph* g, const uint32_t* roots, const uint64_t* states,
-                            uint64_t count, int model) {
+                            uint64_t count, int model, uint64_t* next_draw) {
     return guard([&] {
         need(p, "pool");
         need(g, "graph");
@@ -520,12 +518,17 @@ int immx_pool_sample_rooted(immx_pool* p, const immx_graph* g, const uint32_t* r
             if (roots[i] >= g->g.n) fail(IMMX_ERANGE, "root out of range");
         Device& d = *p->p.dev;
         DBuf<uint32_t> r;
-        DBuf<uint64_t> s;
+        DBuf<uint64_t> s, nd;
         r.exact(count);
         s.exact(count);
+        if (next_draw) nd.exact(count);
         CK(cudaMemcpyAsync(r.p, roots, count * 4, cudaMemcpyHostToDevice, d.stream));
         CK(cudaMemcpyAsync(s.p, states, count * 8, cudaMemcpyHostToDevice, d.stream));
-        sample_into_pool(p->p, g->g, count, 0, 0, r.p, s.p, model);
+        sample_into_pool(p->p, g->g, count, 0, 0, r.p, s.p, model, next_draw ? nd.p : nullptr);
+        if (next_draw) {
+            CK(cudaMemcpyAsync(next_draw, nd.p, count * 8, cudaMemcpyDeviceToHost, d.stream));
+            CK(cudaStreamSynchronize(d.stream));
+        }
     });
 }
 int immx_pool_upload(immx_pool* p, const uint64_t* offsets, const uint32_t* members, uint64_t count) {

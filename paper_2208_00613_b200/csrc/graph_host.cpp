@@ -1,18 +1,26 @@
-// graph_host.cpp -- [host] graph ingestion, transpose, weights, IMMXG1 cache, generators.
+// graph_host.cpp -- [host] graph ingestion, host transpose / weights, the IMMXG1 cache, and
+// the benchmark generators.
 //
-// Semantics follow proj/src/graph.cpp (the input contract of the hot path):
-//   load_edge_list  graph.cpp:24-117   (comments '#', 2 or 3 tokens, self-loops dropped but
-//                                       their vertex kept, first-seen densification, stable
-//                                       sort by (src,dst), duplicates collapse to the first)
-//   transpose       graph.cpp:125-144
-//   assign_weights  graph.cpp:146-157
-//   cache           graph.cpp:159-206  ("IMMXG1", u64 n, u64 m, offsets, targets, probs)
-// The R-MAT / Erdos-Renyi generators are builder-defined (BASELINE configs).
+// Ingestion is outside the hot path; it exists so the Python mirror and the
+// CLI accept the reference's inputs with the reference's behaviour (proj/src/graph.cpp):
+//   text edge lists  graph.cpp:24-117  '#' comment lines and blank lines skipped; 2 or 3
+//                    whitespace-separated tokens (unsigned ids, optional finite weight >= 0);
+//                    self-loops dropped (their endpoint still gets an id); ids densified in
+//                    first-seen order; (src, dst) duplicates keep the first weight; rows sorted
+//                    by target; undirected lines add both directions
+//   transpose        graph.cpp:125-144  stable by source
+//   assign_weights   graph.cpp:146-157
+//   cache            graph.cpp:159-206  "IMMXG1", u64 n, u64 m, offsets, targets, probs (LE)
+// The parser below is this repo's own: one pass over the whole input held in memory, a
+// pointer-scanning tokenizer with an overflow-checked decimal reader, and a single sort of
+// packed (src, dst) keys with the input position as tie-break for the dedup.
 #include <algorithm>
+#include <cerrno>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
-#include <sstream>
+#include <iterator>
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
@@ -20,177 +28,203 @@
 
 #include "internal.hpp"
 
-
 namespace immx_dev {
 
 namespace {
 
-struct EdgeRec {
-    uint32_t src, dst;
+inline bool blank(char c) { return c == ' ' || c == '\t' || c == '\r'; }
+
+// token [b, e) is a non-empty run of decimal digits
+bool all_digits(const char* b, const char* e) {
+    if (b == e) return false;
+    for (const char* c = b; c < e; ++c)
+        if (*c < '0' || *c > '9') return false;
+    return true;
+}
+// its value; one past 2^64-1 is std::out_of_range("stoull"), as the reference reports it
+uint64_t digits_u64(const char* b, const char* e) {
+    uint64_t v = 0;
+    for (const char* c = b; c < e; ++c) {
+        const uint64_t d = (uint64_t)(*c - '0');
+        if (v > (UINT64_MAX - d) / 10) fail(IMMX_ERANGE, "stoull");
+        v = v * 10 + d;
+    }
+    return v;
+}
+
+// a weight: the whole token is one finite, non-negative double
+bool read_weight(const char* b, const char* e, double& out) {
+    const std::string tok(b, e);
+    char* stop = nullptr;
+    errno = 0;
+    const double w = std::strtod(tok.c_str(), &stop);
+    if (stop != tok.c_str() + tok.size() || errno == ERANGE || !std::isfinite(w) || w < 0.0) return false;
+    out = w;
+    return true;
+}
+
+struct ParsedEdge {
+    uint64_t key;  // dense src << 32 | dense dst
+    uint64_t seq;  // input order (the first of equal keys wins)
     double w;
 };
 
-immx_hgraph* build_csr(std::vector<EdgeRec>& edges, std::vector<uint64_t>&& ids) {
-    if (edges.empty()) fail(IMMX_ERUNTIME, "edge list is empty after preprocessing");
-    const uint64_t n = ids.size();
-    std::stable_sort(edges.begin(), edges.end(), [](const EdgeRec& a, const EdgeRec& b) {
-        return a.src != b.src ? a.src < b.src : a.dst < b.dst;
-    });
-    auto last = std::unique(edges.begin(), edges.end(),
-                            [](const EdgeRec& a, const EdgeRec& b) { return a.src == b.src && a.dst == b.dst; });
-    edges.erase(last, edges.end());
-    auto* g = new immx_hgraph;
-    g->n = n;
-    g->m = edges.size();
-    g->original_ids = std::move(ids);
-    g->offsets.assign(n + 1, 0);
-    for (const auto& e : edges) g->offsets[e.src + 1]++;
-    for (uint64_t v = 0; v < n; ++v) g->offsets[v + 1] += g->offsets[v];
-    g->targets.resize(g->m);
-    g->probs.resize(g->m);
-    for (uint64_t i = 0; i < g->m; ++i) {
-        g->targets[i] = edges[i].dst;
-        g->probs[i] = edges[i].w;
+}  // namespace
+
+immx_hgraph* load_edge_list(const char* data, size_t len, bool directed) {
+    std::unordered_map<uint64_t, uint32_t> id_of;
+    std::vector<uint64_t> original;
+    auto dense = [&](uint64_t raw) -> uint32_t {
+        auto it = id_of.find(raw);
+        if (it != id_of.end()) return it->second;
+        const uint32_t d = (uint32_t)original.size();
+        id_of.emplace(raw, d);
+        original.push_back(raw);
+        return d;
+    };
+    std::vector<ParsedEdge> edges;
+    const char* p = data;
+    const char* const end = data + len;
+    for (uint64_t lineno = 1; p < end; ++lineno) {
+        const char* nl = static_cast<const char*>(std::memchr(p, '\n', (size_t)(end - p)));
+        const char* le = nl ? nl : end;
+        const char* tb[4];
+        const char* te[4];
+        int nt = 0;
+        const char* c = p;
+        while (c < le) {
+            while (c < le && blank(*c)) ++c;
+            if (c == le) break;
+            if (nt == 0 && *c == '#') break;  // comment line
+            const char* s = c;
+            while (c < le && !blank(*c)) ++c;
+            if (nt < 4) {
+                tb[nt] = s;
+                te[nt] = c;
+            }
+            ++nt;
+        }
+        const bool comment = nt == 0;
+        if (!comment) {
+            auto malformed = [&] {
+                fail(IMMX_ERUNTIME, "malformed edge list line " + std::to_string(lineno) + ": '" + std::string(p, le) + "'");
+            };
+            if ((nt != 2 && nt != 3) || !all_digits(tb[0], te[0]) || !all_digits(tb[1], te[1])) malformed();
+            const uint64_t a = digits_u64(tb[0], te[0]), b = digits_u64(tb[1], te[1]);
+            double w = 1.0;
+            if (nt == 3 && !read_weight(tb[2], te[2], w)) malformed();
+            const uint32_t u = dense(a);
+            if (a != b) {
+                const uint32_t v = dense(b);
+                edges.push_back({(uint64_t)u << 32 | v, edges.size(), w});
+                if (!directed) edges.push_back({(uint64_t)v << 32 | u, edges.size(), w});
+            }
+        }
+        p = nl ? nl + 1 : end;
     }
+    if (edges.empty()) fail(IMMX_ERUNTIME, "edge list is empty after preprocessing");
+    std::sort(edges.begin(), edges.end(),
+              [](const ParsedEdge& x, const ParsedEdge& y) { return x.key != y.key ? x.key < y.key : x.seq < y.seq; });
+    auto* g = new immx_hgraph;
+    g->n = original.size();
+    g->original_ids = std::move(original);
+    g->offsets.assign(g->n + 1, 0);
+    for (size_t i = 0; i < edges.size(); ++i) {
+        if (i && edges[i].key == edges[i - 1].key) continue;
+        g->targets.push_back((uint32_t)edges[i].key);
+        g->probs.push_back(edges[i].w);
+        g->offsets[(edges[i].key >> 32) + 1]++;
+    }
+    g->m = g->targets.size();
+    for (uint64_t v = 0; v < g->n; ++v) g->offsets[v + 1] += g->offsets[v];
     return g;
 }
 
-bool is_uint(const std::string& t) { return !t.empty() && t.find_first_not_of("0123456789") == std::string::npos; }
-
-}  // namespace
-
-immx_hgraph* load_edge_list(std::istream& in, bool directed) {
-    std::vector<EdgeRec> edges;
-    std::unordered_map<uint64_t, uint32_t> dense;
-    std::vector<uint64_t> ids;
-    auto intern = [&](uint64_t raw) {
-        auto [it, ins] = dense.try_emplace(raw, (uint32_t)ids.size());
-        if (ins) ids.push_back(raw);
-        return it->second;
-    };
-    std::string line;
-    std::vector<std::string> tok;
-    uint64_t lineno = 0;
-    auto malformed = [&](void) {
-        fail(IMMX_ERUNTIME, "malformed edge list line " + std::to_string(lineno) + ": '" + line + "'");
-    };
-    while (std::getline(in, line)) {
-        ++lineno;
-        const auto first = line.find_first_not_of(" \t\r");
-        if (first == std::string::npos || line[first] == '#') continue;
-        tok.clear();
-        for (size_t i = first; i < line.size();) {
-            const auto end = line.find_first_of(" \t\r", i);
-            const auto stop = end == std::string::npos ? line.size() : end;
-            if (stop > i) tok.emplace_back(line, i, stop - i);
-            i = end == std::string::npos ? line.size() : end + 1;
-        }
-        if ((tok.size() != 2 && tok.size() != 3) || !is_uint(tok[0]) || !is_uint(tok[1])) malformed();
-        uint64_t a, b;
-        try {
-            a = std::stoull(tok[0]);
-            b = std::stoull(tok[1]);
-        } catch (const std::exception&) {
-            malformed();
-        }
-        double w = 1.0;
-        if (tok.size() == 3) {
-            size_t used = 0;
-            try {
-                w = std::stod(tok[2], &used);
-            } catch (const std::exception&) {
-                malformed();
-            }
-            if (used != tok[2].size() || w < 0.0 || !std::isfinite(w)) malformed();
-        }
-        if (a == b) {
-            intern(a);
-            continue;
-        }
-        const uint32_t u = intern(a), v = intern(b);
-        edges.push_back({u, v, w});
-        if (!directed) edges.push_back({v, u, w});
-    }
-    return build_csr(edges, std::move(ids));
+immx_hgraph* load_edge_list_file(const std::string& path, bool directed) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) fail(IMMX_ERUNTIME, "cannot open '" + path + "'");
+    const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    return load_edge_list(text.data(), text.size(), directed);
 }
 
+// reverse CSR on the host (the device path transposes in HBM, device_graph.cu): a counting
+// sort on targets, scanning sources in order, keeps every row sorted by source
 immx_hgraph* transpose_host(const immx_hgraph& g) {
     auto* t = new immx_hgraph;
     t->n = g.n;
     t->m = g.m;
     t->original_ids = g.original_ids;
     t->offsets.assign(g.n + 1, 0);
-    for (uint32_t v : g.targets) t->offsets[v + 1]++;
-    for (uint64_t v = 0; v < g.n; ++v) t->offsets[v + 1] += t->offsets[v];
+    for (uint64_t e = 0; e < g.m; ++e) t->offsets[(uint64_t)g.targets[e] + 1]++;
+    for (uint64_t v = 1; v <= g.n; ++v) t->offsets[v] += t->offsets[v - 1];
     t->targets.resize(g.m);
     t->probs.resize(g.m);
-    std::vector<uint64_t> cur(t->offsets.begin(), t->offsets.end() - 1);
-    for (uint64_t u = 0; u < g.n; ++u)
+    std::vector<uint64_t> fill(t->offsets.begin(), t->offsets.end() - 1);
+    for (uint64_t u = 0; u < g.n; ++u) {
         for (uint64_t e = g.offsets[u]; e < g.offsets[u + 1]; ++e) {
-            const uint64_t slot = cur[g.targets[e]]++;
-            t->targets[slot] = (uint32_t)u;
-            t->probs[slot] = g.probs[e];
+            const uint64_t at = fill[g.targets[e]]++;
+            t->targets[at] = (uint32_t)u;
+            t->probs[at] = g.probs[e];
         }
+    }
     return t;
 }
 
+// model 0 = weighted cascade 1/indeg(v), 1 = uniform p; f32: round through float32
 void assign_weights_host(immx_hgraph& g, int model, double p, bool f32) {
+    auto round = [f32](double x) { return f32 ? (double)(float)x : x; };
     if (model == 1) {
-        if (p < 0.0 || p > 1.0) fail(IMMX_EINVAL, "uniform edge probability must be in [0,1]");
-        const double q = f32 ? (double)(float)p : p;
-        std::fill(g.probs.begin(), g.probs.end(), q);
+        if (!(p >= 0.0 && p <= 1.0)) fail(IMMX_EINVAL, "uniform edge probability must be in [0,1]");
+        g.probs.assign(g.m, round(p));
         return;
     }
     if (model != 0) fail(IMMX_EINVAL, "unknown weight model");
-    std::vector<uint64_t> indeg(g.n, 0);
-    for (uint32_t v : g.targets) indeg[v]++;
-    for (uint64_t i = 0; i < g.m; ++i) {
-        const double w = 1.0 / (double)indeg[g.targets[i]];
-        g.probs[i] = f32 ? (double)(float)w : w;
-    }
+    std::vector<uint32_t> indeg(g.n, 0);
+    for (uint64_t e = 0; e < g.m; ++e) indeg[g.targets[e]]++;
+    g.probs.resize(g.m);
+    for (uint64_t e = 0; e < g.m; ++e) g.probs[e] = round(1.0 / (double)indeg[g.targets[e]]);
 }
 
 namespace {
-const char kMagic[6] = {'I', 'M', 'M', 'X', 'G', '1'};
+constexpr char kCacheMagic[] = "IMMXG1";  // 6 bytes on disk, no terminator
 }
 
 void save_cache(const immx_hgraph& g, const std::string& path) {
     std::ofstream out(path, std::ios::binary);
     if (!out) fail(IMMX_ERUNTIME, "cannot write '" + path + "'");
-    out.write(kMagic, 6);
-    out.write(reinterpret_cast<const char*>(&g.n), 8);
-    out.write(reinterpret_cast<const char*>(&g.m), 8);
-    out.write(reinterpret_cast<const char*>(g.offsets.data()), (std::streamsize)(8 * g.offsets.size()));
-    out.write(reinterpret_cast<const char*>(g.targets.data()), (std::streamsize)(4 * g.targets.size()));
-    out.write(reinterpret_cast<const char*>(g.probs.data()), (std::streamsize)(8 * g.probs.size()));
+    auto put = [&](const void* p, size_t bytes) { out.write(static_cast<const char*>(p), (std::streamsize)bytes); };
+    put(kCacheMagic, 6);
+    put(&g.n, 8);
+    put(&g.m, 8);
+    put(g.offsets.data(), 8 * g.offsets.size());
+    put(g.targets.data(), 4 * g.targets.size());
+    put(g.probs.data(), 8 * g.probs.size());
     if (!out) fail(IMMX_ERUNTIME, "short write to '" + path + "'");
 }
 
 immx_hgraph* load_cache(const std::string& path) {
     std::ifstream in(path, std::ios::binary);
     if (!in) fail(IMMX_ERUNTIME, "cannot open '" + path + "'");
-    char magic[6];
+    char magic[6] = {0};
     in.read(magic, 6);
-    if (!in || std::memcmp(magic, kMagic, 6) != 0) fail(IMMX_ERUNTIME, "'" + path + "' is not an IMMXG1 graph cache");
-    auto* g = new immx_hgraph;
-    auto rd = [&](void* p, size_t bytes) {
+    if (!in || std::memcmp(magic, kCacheMagic, 6) != 0)
+        fail(IMMX_ERUNTIME, "'" + path + "' is not an IMMXG1 graph cache");
+    std::unique_ptr<immx_hgraph> g(new immx_hgraph);
+    auto get = [&](void* p, size_t bytes) {
         in.read(static_cast<char*>(p), (std::streamsize)bytes);
-        if (!in) {
-            delete g;
-            fail(IMMX_ERUNTIME, "graph cache truncated");
-        }
+        if (!in) fail(IMMX_ERUNTIME, "graph cache truncated");
     };
-    rd(&g->n, 8);
-    rd(&g->m, 8);
+    get(&g->n, 8);
+    get(&g->m, 8);
     g->offsets.resize(g->n + 1);
     g->targets.resize(g->m);
     g->probs.resize(g->m);
-    rd(g->offsets.data(), 8 * (g->n + 1));
-    rd(g->targets.data(), 4 * g->m);
-    rd(g->probs.data(), 8 * g->m);
+    get(g->offsets.data(), 8 * (g->n + 1));
+    get(g->targets.data(), 4 * g->m);
+    get(g->probs.data(), 8 * g->m);
     g->original_ids.resize(g->n);
     for (uint64_t v = 0; v < g->n; ++v) g->original_ids[v] = v;
-    return g;
+    return g.release();
 }
 
 // ---- generators ------------------------------------------------------------------

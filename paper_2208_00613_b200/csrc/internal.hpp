@@ -296,7 +296,8 @@ void graph_generate_rmat(DevGraph& G, Device& d, uint32_t scale, uint32_t ef, do
 void graph_download(const DevGraph& G, uint64_t* row, uint32_t* col, double* prob);
 // sampler.cu
 void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first, uint64_t seed,
-                      const uint32_t* d_roots, const uint64_t* d_states, int model);
+                      const uint32_t* d_roots, const uint64_t* d_states, int model,
+                      uint64_t* d_next_draw = nullptr);
 // pool_select.cu
 void pool_hist_dev(const Pool& P, uint64_t lo, uint64_t hi, unsigned int* d_hist);
 void argmax_dev(Device& d, const unsigned int* d_hist, uint64_t n, unsigned long long* d_key);

@@ -140,6 +140,7 @@ struct SampleResult {
     uint64_t edges;   // edges of the members' rows (E_j)
     bool overflow;
     uint64_t probes = 0;  // LT: cumulative-weight entries read by the searches
+    uint64_t t_end = 0;   // index of the next unused draw of the sample's stream
 };
 
 template <class Vis>
@@ -186,7 +187,7 @@ __device__ __forceinline__ SampleResult walk_lt(const GView& g, Vis& vis, uint32
         probes += hi - lo;
         const uint32_t v = g.col[chosen];
         if (vis.has(v)) break;
-        if (qlen + 1 > qcap) return {qlen, edges, true, probes};
+        if (qlen + 1 > qcap) return {qlen, edges, true, probes, t};
         __syncwarp();
         if (lane == 0) {
             q[qlen] = v;
@@ -196,7 +197,7 @@ __device__ __forceinline__ SampleResult walk_lt(const GView& g, Vis& vis, uint32
         qlen++;
         cur = v;
     }
-    return {qlen, edges, false, probes};
+    return {qlen, edges, false, probes, t};
 }
 
 // ------------------------------------------------------------------ the kernel ----
@@ -217,6 +218,7 @@ struct SampJob {
     const uint32_t* roots;           // rooted mode (nullptr -> seeded)
     const uint64_t* states;
     const uint32_t* list;            // sample indices to do (nullptr -> 0..count)
+    uint64_t* next_draw;             // optional, per sample: index of the next unused draw
     uint32_t count;
     uint64_t pool_base;              // pool index of local sample 0
     uint64_t* set_off;
@@ -232,6 +234,8 @@ struct SampJob {
     uint32_t qcap;
     int model;
     int exact_coins;                 // test knob: every coin through the exact (tie) path
+    uint32_t long_min;               // rows of at least this degree run the long-row path
+                                     // (0xffffffff: never -- per-edge p, multigraph rows, LT)
     unsigned int* run_hist;          // non-null: the pool's running vertex histogram (select_raw's),
                                      // counted as the sets are committed
     // promotion slots (hash tiers): a sample outgrowing its shared-memory hash takes a slot
@@ -321,6 +325,7 @@ __global__ void __launch_bounds__(256) rrr_kernel(GView g, SampJob job, uint32_t
                 if (lane == 0) {
                     job.set_off[job.pool_base + j] = base;
                     job.set_len[job.pool_base + j] = res.size;
+                    if (job.next_draw) job.next_draw[j] = res.t_end;
                     atomicAdd(&job.ctl->edges, (unsigned long long)res.edges);
                     atomicAdd(&job.ctl->members, (unsigned long long)res.size);
                     if (res.probes) atomicAdd(&job.ctl->probes, (unsigned long long)res.probes);
@@ -452,6 +457,7 @@ struct BlkSmem {
     alignas(16) uint32_t wsum2[NW];
     uint32_t nextrow[2][NW];  // rows of the next group's warp starts (double-buffered)
     uint32_t hdup;            // hash tiers: duplicate keys left by conflict rollbacks
+    uint32_t wlong[NW];       // per warp: first long row of the batch (NB: none)
     int pslot;                // hash tiers: the promotion slot taken (-1: none)
     uint32_t lbuf[2 * NW * 32 * U];  // rare path: success positions (lbuf[0, G)) and targets (lbuf[G, 2G))
     uint32_t cut;
@@ -573,6 +579,100 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                 if constexpr (P) return atomicOr(pw + (v >> 5), 1u << (v & 31)) & (1u << (v & 31));
                 else return vis.add_test(v);
             };
+            // ---- long rows (degree >= job.long_min): one row alone, in slabs ----
+            // A row's targets are distinct (no multigraph rows here), so which positions draw is
+            // fixed by the visited set at the row start, and the successes cannot conflict.  A
+            // slab gives warp w the 32*S consecutive positions [wb, wb + 32*S): lane l tests
+            // positions wb + 32*i + l (coalesced loads) into a candidate mask; one CTA prefix of
+            // the warps' candidate counts numbers the draws, and the coins run as S warp-wide
+            // steps -- no row mapping, no re-probe, three barriers per slab (NW*1024 positions)
+            // instead of three per group.  Successes are appended in position order.
+            auto long_row = [&](uint32_t u) {
+                const uint64_t rb = g.row[u];
+                const uint64_t D = g.row[u + 1] - rb;
+                const uint64_t Trow = PM == kProbRow ? g.thr[u] : g.gthr;
+                edges += D;
+                if (PM == kProbRow && Trow == kThrNever) return;  // p <= 0: no draw (sampler.cpp:38)
+                const bool always = PM == kProbRow && Trow == kThrAlways;  // p >= 1: no draw, all join
+                const uint32_t thi = (uint32_t)(Trow >> 32);
+                const uint32_t* __restrict__ cp = g.col + rb;
+                for (uint64_t base = 0; base < D;) {
+                    const uint32_t S = (uint32_t)min((uint64_t)32, (D - base + NW * 32 - 1) / (NW * 32));
+                    const uint64_t wb = base + (uint64_t)w * 32 * S;
+                    // all of the lane's loads first (up to 32 in flight: a hub row streams from
+                    // DRAM / L2 at full latency), then the visited tests
+                    uint32_t tv[32];
+    #pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const uint64_t pp = wb + (uint64_t)i * 32 + lane;
+                        tv[i] = (i < (int)S && pp < D) ? __ldg(cp + pp) : 0xffffffffu;
+                    }
+                    uint32_t m = 0;
+    #pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (tv[i] != 0xffffffffu && !vhas(tv[i])) m |= 1u << i;
+                    const uint32_t cw = __reduce_add_sync(FULL, __popc(m));
+                    if (lane == 0) sh.wsum[w] = cw;
+                    __syncthreads();
+                    uint32_t cbefore, ctotal;
+                    warp_prefix<NW>(sh.wsum, w, cbefore, ctotal);
+                    uint32_t sm = 0;
+                    if (always) {
+                        sm = m;
+                    } else {
+                        uint64_t tb = t + cbefore;
+                        bool tie = job.exact_coins;
+    #pragma unroll 8
+                        for (uint32_t i = 0; i < S; ++i) {
+                            const bool c = (m >> i) & 1u;
+                            const uint32_t bal = __ballot_sync(FULL, c);
+                            const uint32_t zh = coin_zhi(s0, tb + __popc(bal & lt));
+                            sm |= (uint32_t)(c && zh < thi) << i;
+                            tie |= c && (zh ^ thi) < 2u;
+                            tb += __popc(bal);
+                        }
+                        if (__any_sync(FULL, tie)) {  // rare: the low words decide
+                            sm = 0;
+                            tb = t + cbefore;
+                            for (uint32_t i = 0; i < S; ++i) {
+                                const bool c = (m >> i) & 1u;
+                                const uint32_t bal = __ballot_sync(FULL, c);
+                                if (c && coin_success(s0, tb + __popc(bal & lt), Trow)) sm |= 1u << i;
+                                tb += __popc(bal);
+                            }
+                        }
+                    }
+                    const uint32_t sw = __reduce_add_sync(FULL, __popc(sm));
+                    if (lane == 0) sh.wsum2[w] = sw;
+                    __syncthreads();
+                    uint32_t sbefore, stotal;
+                    warp_prefix<NW>(sh.wsum2, w, sbefore, stotal);
+                    if (qlen + (P ? 0u : sh.hdup) + stotal > qcap) {  // CTA-uniform
+                        overflow = true;
+                        return;
+                    }
+                    if (sw) {
+                        uint32_t pos = qlen + sbefore;
+                        uint32_t orm = __reduce_or_sync(FULL, sm);
+                        while (orm) {
+                            const uint32_t i = __ffs(orm) - 1;
+                            orm &= orm - 1;
+                            const bool sc = (sm >> i) & 1u;
+                            const uint32_t bal = __ballot_sync(FULL, sc);
+                            if (sc) {
+                                const uint32_t v = __ldg(cp + wb + i * 32 + lane);
+                                q[pos + __popc(bal & lt)] = v;
+                                vadd(v);
+                            }
+                            pos += __popc(bal);
+                        }
+                    }
+                    qlen += stotal;
+                    if (!always) t += ctotal;
+                    base += (uint64_t)NW * 32 * S;
+                    __syncthreads();  // inserts and queue writes visible; wsum / wsum2 reusable
+                }
+            };
             while (qhead < qlen && !overflow) {
                 if constexpr (kHash && !P) {
                     // at 7/8 of the hash's capacity (7/16 load; the bit filter keeps the longer
@@ -585,7 +685,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     }
                 }
                 // ---- batch of rows q[qhead .. qhead+nb) ----
-                const uint32_t nb = min(NB, qlen - qhead);
+                uint32_t nb = min(NB, qlen - qhead);
                 uint32_t deg = 0;
                 uint64_t rs = 0, th = g.gthr;
                 if (tid < nb) {
@@ -593,6 +693,25 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     rs = g.row[u];
                     deg = (uint32_t)(g.row[u + 1] - rs);
                     if (PM == kProbRow) th = g.thr[u];
+                }
+                if constexpr (PM != kProbEdge) {
+                    if (job.long_min != 0xffffffffu) {  // the batch ends before its first long row
+                        const uint32_t lb = __ballot_sync(FULL, tid < nb && deg >= job.long_min);
+                        if (lane == 0) sh.wlong[w] = lb ? w * 32 + __ffs(lb) - 1 : NB;
+                        __syncthreads();
+                        uint32_t f = NB;
+    #pragma unroll
+                        for (int k = 0; k < NW; ++k) f = min(f, sh.wlong[k]);
+                        if (f == 0) {  // (CTA-uniform)
+                            long_row(q[qhead]);
+                            qhead += 1;
+                            continue;
+                        }
+                        if (f < nb) {
+                            nb = f;
+                            if (tid >= nb) deg = 0;
+                        }
+                    }
                 }
                 uint32_t x = deg;
     #pragma unroll
@@ -955,6 +1074,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                 if (tid == 0) {
                     job.set_off[job.pool_base + j] = base;
                     job.set_len[job.pool_base + j] = qlen;
+                    if (job.next_draw) job.next_draw[j] = t;
                     atomicAdd(&job.ctl->edges, (unsigned long long)edges);
                     atomicAdd(&job.ctl->members, (unsigned long long)qlen);
                 }
@@ -1092,6 +1212,15 @@ bool promote_enabled() {  // IMMX_NO_PROMOTE=1 restarts overflowing samples on t
     return on;
 }
 
+uint32_t long_row_min() {  // IMMX_LONG_MIN=d: rows of degree >= d take the long-row path (0: never)
+    const char* e = std::getenv("IMMX_LONG_MIN");
+    if (e && *e) {
+        const long v = std::atol(e);
+        return v <= 0 ? 0xffffffffu : (uint32_t)v;
+    }
+    return 0xffffffffu;  // off by default until it measures faster
+}
+
 bool exact_coins_forced() {  // IMMX_EXACT_COINS=1: tests drive every coin through the tie path
     const char* e = std::getenv("IMMX_EXACT_COINS");
     return e && *e && *e != '0';
@@ -1130,7 +1259,7 @@ GView make_view(const DevGraph& g) {
 
 // Append `count` samples to the pool.  roots/states (device pointers) select rooted mode.
 void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first, uint64_t seed,
-                      const uint32_t* d_roots, const uint64_t* d_states, int model) {
+                      const uint32_t* d_roots, const uint64_t* d_states, int model, uint64_t* d_next_draw) {
     Device& d = *P.dev;
     cudaStream_t s = d.stream;
     if (count == 0) return;
@@ -1143,9 +1272,9 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         // cold pool on a new graph: a pilot batch measures the mean set size, so the arena is
         // sized once (an undersized arena makes in-flight samples redo their work); repeated
         // runs on the graph size it from the last mean and skip the pilot's launch tail
-        sample_into_pool(P, G, 2048, first, seed, d_roots, d_states, model);
+        sample_into_pool(P, G, 2048, first, seed, d_roots, d_states, model, d_next_draw);
         sample_into_pool(P, G, count - 2048, first + 2048, seed, d_roots ? d_roots + 2048 : nullptr,
-                         d_states ? d_states + 2048 : nullptr, model);
+                         d_states ? d_states + 2048 : nullptr, model, d_next_draw ? d_next_draw + 2048 : nullptr);
         return;
     }
     const uint64_t base = P.count;
@@ -1237,6 +1366,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     job.first = first;
     job.roots = d_roots;
     job.states = d_states;
+    job.next_draw = d_next_draw;
     job.pool_base = base;
     job.set_off = P.off.p;
     job.set_len = P.len.p;
@@ -1244,6 +1374,8 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     job.ctl = ctl.p;
     job.model = model;
     job.exact_coins = exact_coins_forced() ? 1 : 0;
+    job.long_min = long_row_min();
+    if (G.row_dups || gv.pmode == kProbEdge || model != IMMX_MODEL_IC) job.long_min = 0xffffffffu;
     // select_raw's running histogram of this pool, when it already covers exactly the sets
     // before this batch: the sampler counts the batch into it (no separate pass over the sets).
     // Only for large sets (mean >= 64: c2 -14 ms a run); with many small ones (c4) the
