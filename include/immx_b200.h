@@ -110,7 +110,11 @@ IMMX_API int immx_codebook_build(const uint64_t* freq, uint64_t n, uint64_t* cod
 
 /* ---------------------------------------------------------------- device context --- */
 IMMX_API int immx_device_create(int ordinal, immx_device** out);
-IMMX_API void immx_device_destroy(immx_device* d);
+IMMX_API void immx_device_destroy(immx_device* d);         /* no-op on the shared device */
+/* The process's shared context (created on first use, lives for the process): what the
+ * Python package and a reference build linked on this library both use,
+ * so they can run in one process.  A context from immx_device_create is exclusive. */
+IMMX_API int immx_device_shared(int ordinal, immx_device** out);
 IMMX_API void* immx_device_stream(immx_device* d);            /* the cudaStream_t all calls use */
 IMMX_API int immx_device_synchronize(immx_device* d);
 IMMX_API uint64_t immx_device_kernel_launches(const immx_device* d); /* our kernels launched so far */

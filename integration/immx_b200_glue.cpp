@@ -45,7 +45,7 @@ void b200_check(int s) {
 immx_device* b200_device() {  // one context + stream per process
     static immx_device* d = [] {
         immx_device* h = nullptr;
-        b200_check(immx_device_create(0, &h));
+        b200_check(immx_device_shared(0, &h));  // the process's context (shared with the Python package)
         return h;
     }();
     return d;

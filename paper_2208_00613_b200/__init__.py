@@ -45,9 +45,12 @@ _MODE_NAME = {v: k for k, v in _MODE_ID.items()}
 class Device:
     """One CUDA context + stream (immx_device)."""
 
-    def __init__(self, ordinal: int = 0):
+    def __init__(self, ordinal: int = 0, shared: bool = False):
+        """shared=True: the process's shared context (immx_device_shared), which other users
+        of the library in this process -- e.g. the reference module rebuilt on it
+        (integration/) -- see too; otherwise an exclusive one."""
         h = C.c_void_p()
-        check(lib.immx_device_create(ordinal, C.byref(h)))
+        check((lib.immx_device_shared if shared else lib.immx_device_create)(ordinal, C.byref(h)))
         self.h = h
         self.ordinal = ordinal
 
@@ -90,7 +93,7 @@ def default_device(ordinal: int | None = None) -> Device:
     """The process's immx_device (the C-ABI admits one live context per process)."""
     global _DEFAULT
     if _DEFAULT is None:
-        _DEFAULT = Device(0 if ordinal is None else ordinal)
+        _DEFAULT = Device(0 if ordinal is None else ordinal, shared=True)
     elif ordinal is not None and ordinal != _DEFAULT.ordinal:
         raise ValueError(f"the process already uses cuda:{_DEFAULT.ordinal} (one immx_device per process)")
     return _DEFAULT

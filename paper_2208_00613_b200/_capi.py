@@ -95,6 +95,7 @@ SIGNATURES = {
     "immx_codebook_build": (I, [pu64, u64, pu64, pu8, pu64]),
     "immx_device_create": (I, [I, PP]),
     "immx_device_destroy": (None, [P]),
+    "immx_device_shared": (I, [I, PP]),
     "immx_device_stream": (P, [P]),
     "immx_device_synchronize": (I, [P]),
     "immx_device_kernel_launches": (u64, [P]),

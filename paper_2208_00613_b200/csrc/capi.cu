@@ -16,6 +16,7 @@
 #include <memory>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <fstream>
 #include <sstream>
 #include <string>
@@ -370,8 +371,28 @@ int immx_device_create(int ordinal, immx_device** out) {
         *out = h;
     });
 }
+int immx_device_shared(int ordinal, immx_device** out) {
+    // one context per process, shared by every caller in it (the Python package, a rebuilt
+    // reference module, ...); created on first use, never destroyed
+    static std::mutex mu;
+    static immx_device* shared = nullptr;
+    return guard([&] {
+        need(out, "out");
+        std::lock_guard<std::mutex> lk(mu);
+        if (!shared) {
+            immx_device* h = nullptr;
+            const int rc = immx_device_create(ordinal, &h);
+            if (rc != IMMX_OK) fail(rc, immx_last_error());
+            h->shared = true;
+            shared = h;
+        } else if (shared->d.ordinal != ordinal) {
+            fail(IMMX_EINVAL, "the process's shared immx_device is on another ordinal");
+        }
+        *out = shared;
+    });
+}
 void immx_device_destroy(immx_device* h) {
-    if (!h) return;
+    if (!h || h->shared) return;
     cudaStreamSynchronize(h->d.stream);
     if (h->d.host_scal) cudaFreeHost(h->d.host_scal);
     delete h->d.run_pool;

@@ -412,6 +412,7 @@ void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& l
 
 struct immx_device {
     immx_dev::Device d;
+    bool shared = false;  // immx_device_shared's context: lives for the process
 };
 struct immx_graph {
     immx_dev::DevGraph g;

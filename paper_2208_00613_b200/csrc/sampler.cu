@@ -35,6 +35,12 @@
 #ifndef IMMX_MINB
 #define IMMX_MINB 5  // resident 8-warp CTAs per SM the register budget is set for (global / per-edge p)
 #endif
+#ifndef IMMX_LONG_MIN_DEFAULT
+#define IMMX_LONG_MIN_DEFAULT 4096  // rows of at least this degree take the long-row path
+#endif
+#ifndef IMMX_LONG_LR
+#define IMMX_LONG_LR 16  // positions per thread per long-row slab (multiple of 4, <= 32)
+#endif
 #ifndef IMMX_MINB_ROW
 #define IMMX_MINB_ROW 4  // the same with per-row p (its row-threshold array leaves room for 4)
 #endif
@@ -74,6 +80,16 @@ __device__ __forceinline__ bool coin_success(uint64_t s0, uint64_t t, uint64_t t
     const uint32_t xlo = zlo ^ ((zlo >> 31) | (zhi << 1));
     return xlo < (uint32_t)tsh;
 }
+
+// The same two tests on the draw's pre-mix value z = s0 + t * kGamma (callers that walk
+// consecutive draws keep z running instead of multiplying t).
+__device__ __forceinline__ uint32_t zhi_of(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    const uint64_t y = z ^ (z >> 27);
+    const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
+    return __umulhi(ylo, 0x133111ebu) + ylo * 0x94d049bbu + yhi * 0x133111ebu;
+}
+__device__ __forceinline__ bool success_of(uint64_t z, uint64_t tsh) { return coin_success(z, 0, tsh); }
 
 // High word of the draw before splitmix64's last step (x = z ^ (z >> 31)), zhi.  The last step
 // flips bit 0 of the high word when bit 31 is set, so x < (T << 11) agrees with zhi < thi (thi
@@ -511,6 +527,11 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
     const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t lt = lanemask_lt();
     constexpr bool kHash = KIND == kBHash13 || KIND == kBHash15;
+    // positions per thread per long-row slab
+    constexpr uint32_t LR = IMMX_LONG_LR;
+    // a promoted sample's filter: one bit per vertex hash over the idle hash slots (2^(LOGH+5) bits)
+    constexpr uint32_t LOGPF = (KIND == kBHash15 ? 15 : 13) + 5;
+    auto pf_hash = [](uint32_t v) -> uint32_t { return (v * 0x2C1B3C6Du) >> (32 - LOGPF); };
     // invalid positions (past the batch) load the root instead of being tested: fewer integer
     // instructions, but one more live register -- a loss at the global-p kernels' 48 registers
     constexpr bool kRootFill = PM != kProbGlobal;
@@ -576,17 +597,43 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                 else return vis.has(v);
             };
             auto vadd = [&](uint32_t v) -> bool {
-                if constexpr (P) return atomicOr(pw + (v >> 5), 1u << (v & 31)) & (1u << (v & 31));
-                else return vis.add_test(v);
+                if constexpr (P) {
+                    const uint32_t b = pf_hash(v);  // the promoted sample's filter (long rows)
+                    atomicOr(&dsm[b >> 5], 1u << (b & 31));
+                    return atomicOr(pw + (v >> 5), 1u << (v & 31)) & (1u << (v & 31));
+                } else {
+                    return vis.add_test(v);
+                }
+            };
+            // long-row visited tests: a first, branch-free step (a filter bit where the set is a
+            // hash or a promoted sample's global bitmap, else the exact bit), then the exact test
+            constexpr bool kTwoStep = P || kHash;
+            auto lmaybe = [&](uint32_t v) -> bool {
+                if constexpr (P) {
+                    const uint32_t b = pf_hash(v);
+                    return (dsm[b >> 5] >> (b & 31)) & 1u;
+                } else if constexpr (kHash) {
+                    return vis.maybe(v);
+                } else {
+                    return vis.has(v);
+                }
+            };
+            auto lexact = [&](uint32_t v) -> bool {
+                if constexpr (P) return (__ldcg(pw + (v >> 5)) >> (v & 31)) & 1u;
+                else if constexpr (kHash) return vis.probe(v);
+                else return true;
             };
             // ---- long rows (degree >= job.long_min): one row alone, in slabs ----
             // A row's targets are distinct (no multigraph rows here), so which positions draw is
-            // fixed by the visited set at the row start, and the successes cannot conflict.  A
-            // slab gives warp w the 32*S consecutive positions [wb, wb + 32*S): lane l tests
-            // positions wb + 32*i + l (coalesced loads) into a candidate mask; one CTA prefix of
-            // the warps' candidate counts numbers the draws, and the coins run as S warp-wide
-            // steps -- no row mapping, no re-probe, three barriers per slab (NW*1024 positions)
-            // instead of three per group.  Successes are appended in position order.
+            // fixed by the visited set at the row start and the successes cannot conflict: the
+            // row needs no conflict check, no re-probe and no row mapping.  A slab gives thread
+            // `tid` the LR consecutive positions [tid*LR, tid*LR + LR) (from the row start
+            // rounded down to 16 bytes; 128-bit loads), tested against the visited set into a
+            // candidate mask; a warp scan and one CTA prefix of the candidate counts number the
+            // draws, and the lane runs its coins in position order on the running pre-mix value
+            // z = s0 + t*gamma (one 64-bit add per candidate instead of a multiply).  Successes
+            // (~1 per weighted-cascade row) reload their target and are appended in position
+            // order after a second prefix.  Two barriers per slab of NW*32*LR positions.
             auto long_row = [&](uint32_t u) {
                 const uint64_t rb = g.row[u];
                 const uint64_t D = g.row[u + 1] - rb;
@@ -595,83 +642,117 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                 if (PM == kProbRow && Trow == kThrNever) return;  // p <= 0: no draw (sampler.cpp:38)
                 const bool always = PM == kProbRow && Trow == kThrAlways;  // p >= 1: no draw, all join
                 const uint32_t thi = (uint32_t)(Trow >> 32);
-                const uint32_t* __restrict__ cp = g.col + rb;
-                for (uint64_t base = 0; base < D;) {
-                    const uint32_t S = (uint32_t)min((uint64_t)32, (D - base + NW * 32 - 1) / (NW * 32));
-                    const uint64_t wb = base + (uint64_t)w * 32 * S;
-                    // all of the lane's loads first (up to 32 in flight: a hub row streams from
-                    // DRAM / L2 at full latency), then the visited tests
-                    uint32_t tv[32];
+                const uint32_t head = (uint32_t)(rb & 3);             // aligned base = rb - head
+                const uint32_t* __restrict__ cb = g.col + (rb - head);
+                const uint64_t span = D + head;
+                constexpr uint32_t SLAB = NW * 32 * LR;
+                for (uint64_t sb = 0; sb < span; sb += SLAB) {
+                    const uint64_t e0 = sb + (uint64_t)tid * LR;  // this thread's first element
+                    uint32_t cm = 0;                              // candidates (bit k: element e0 + k)
+                    if (e0 < span) {
+                        uint32_t v[LR];
+                        uint32_t valid;
+                        if (e0 >= head && e0 + LR <= span) {
+                            const uint4* p4 = reinterpret_cast<const uint4*>(cb + e0);
     #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const uint64_t pp = wb + (uint64_t)i * 32 + lane;
-                        tv[i] = (i < (int)S && pp < D) ? __ldg(cp + pp) : 0xffffffffu;
+                            for (int k = 0; k < (int)LR / 4; ++k) {
+                                const uint4 x = __ldg(p4 + k);
+                                v[4 * k] = x.x;
+                                v[4 * k + 1] = x.y;
+                                v[4 * k + 2] = x.z;
+                                v[4 * k + 3] = x.w;
+                            }
+                            valid = (uint32_t)((1ull << LR) - 1);
+                        } else {
+                            valid = 0;
+    #pragma unroll
+                            for (int k = 0; k < (int)LR; ++k) {
+                                const bool ok = e0 + k >= head && e0 + k < span;
+                                v[k] = ok ? __ldg(cb + e0 + k) : 0u;
+                                valid |= (uint32_t)ok << k;
+                            }
+                        }
+                        // first step, branch-free: a filter bit (hash tiers, promoted samples) or
+                        // the exact bit (bitmap tiers); the rare maybes re-read their target
+                        uint32_t fm = 0;
+    #pragma unroll
+                        for (int k = 0; k < (int)LR; ++k) fm |= (uint32_t)lmaybe(v[k]) << k;
+                        fm &= valid;
+                        cm = valid & ~fm;
+                        if constexpr (kTwoStep) {
+                            while (fm) {
+                                const uint32_t k = __ffs(fm) - 1;
+                                fm &= fm - 1;
+                                if (!lexact(__ldg(cb + e0 + k))) cm |= 1u << k;
+                            }
+                        }
                     }
-                    uint32_t m = 0;
+                    const uint32_t nc = __popc(cm);
+                    uint32_t incl = nc;
     #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (tv[i] != 0xffffffffu && !vhas(tv[i])) m |= 1u << i;
-                    const uint32_t cw = __reduce_add_sync(FULL, __popc(m));
-                    if (lane == 0) sh.wsum[w] = cw;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= (uint32_t)o) incl += y;
+                    }
+                    if (lane == 31) sh.wsum[w] = incl;
                     __syncthreads();
                     uint32_t cbefore, ctotal;
                     warp_prefix<NW>(sh.wsum, w, cbefore, ctotal);
                     uint32_t sm = 0;
                     if (always) {
-                        sm = m;
-                    } else {
-                        uint64_t tb = t + cbefore;
+                        sm = cm;
+                    } else if (cm) {
+                        const uint64_t d0 = t + cbefore + (incl - nc);  // draw number of the first candidate
+                        uint64_t z = s0 + d0 * kGamma;
                         bool tie = job.exact_coins;
-    #pragma unroll 8
-                        for (uint32_t i = 0; i < S; ++i) {
-                            const bool c = (m >> i) & 1u;
-                            const uint32_t bal = __ballot_sync(FULL, c);
-                            const uint32_t zh = coin_zhi(s0, tb + __popc(bal & lt));
-                            sm |= (uint32_t)(c && zh < thi) << i;
-                            tie |= c && (zh ^ thi) < 2u;
-                            tb += __popc(bal);
+    #pragma unroll
+                        for (int k = 0; k < (int)LR; ++k) {
+                            const bool c = (cm >> k) & 1u;
+                            const uint32_t zh = zhi_of(z);
+                            sm |= (uint32_t)(c && zh < thi) << k;
+                            tie |= c && (uint32_t)(zh - thi + 1u) < 3u;  // zh in {thi - 1, thi, thi + 1}
+                            z += c ? kGamma : 0ull;
                         }
-                        if (__any_sync(FULL, tie)) {  // rare: the low words decide
+                        if (tie) {  // rare (~2^-31 a draw): this lane's coins on the full words
                             sm = 0;
-                            tb = t + cbefore;
-                            for (uint32_t i = 0; i < S; ++i) {
-                                const bool c = (m >> i) & 1u;
-                                const uint32_t bal = __ballot_sync(FULL, c);
-                                if (c && coin_success(s0, tb + __popc(bal & lt), Trow)) sm |= 1u << i;
-                                tb += __popc(bal);
+                            z = s0 + d0 * kGamma;
+                            for (uint32_t k = 0; k < LR; ++k) {
+                                if (!((cm >> k) & 1u)) continue;
+                                sm |= (uint32_t)success_of(z, Trow) << k;
+                                z += kGamma;
                             }
                         }
                     }
-                    const uint32_t sw = __reduce_add_sync(FULL, __popc(sm));
+                    const uint32_t ns = __popc(sm);
+                    const uint32_t sw = __reduce_add_sync(FULL, ns);
                     if (lane == 0) sh.wsum2[w] = sw;
                     __syncthreads();
                     uint32_t sbefore, stotal;
                     warp_prefix<NW>(sh.wsum2, w, sbefore, stotal);
                     if (qlen + (P ? 0u : sh.hdup) + stotal > qcap) {  // CTA-uniform
                         overflow = true;
-                        return;
+                        break;
                     }
-                    if (sw) {
-                        uint32_t pos = qlen + sbefore;
-                        uint32_t orm = __reduce_or_sync(FULL, sm);
-                        while (orm) {
-                            const uint32_t i = __ffs(orm) - 1;
-                            orm &= orm - 1;
-                            const bool sc = (sm >> i) & 1u;
-                            const uint32_t bal = __ballot_sync(FULL, sc);
-                            if (sc) {
-                                const uint32_t v = __ldg(cp + wb + i * 32 + lane);
-                                q[pos + __popc(bal & lt)] = v;
-                                vadd(v);
-                            }
-                            pos += __popc(bal);
+                    if (sw) {  // (warp-uniform, rare)
+                        uint32_t sincl = ns;
+    #pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t y = __shfl_up_sync(FULL, sincl, o);
+                            if (lane >= (uint32_t)o) sincl += y;
+                        }
+                        uint32_t pos = qlen + sbefore + sincl - ns;
+                        while (sm) {
+                            const uint32_t k = __ffs(sm) - 1;
+                            sm &= sm - 1;
+                            const uint32_t x = __ldg(cb + e0 + k);
+                            q[pos++] = x;
+                            vadd(x);
                         }
                     }
                     qlen += stotal;
                     if (!always) t += ctotal;
-                    base += (uint64_t)NW * 32 * S;
-                    __syncthreads();  // inserts and queue writes visible; wsum / wsum2 reusable
                 }
+                __syncthreads();  // inserts and queue writes visible to the next row
             };
             while (qhead < qlen && !overflow) {
                 if constexpr (kHash && !P) {
@@ -1042,10 +1123,14 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                 if (sh.pslot >= 0) {
                     uint32_t* nq = job.pq + (size_t)sh.pslot * job.pqcap;
                     uint32_t* nw = job.pbits + (size_t)sh.pslot * job.pwords;
+                    for (uint32_t k = tid; k < (1u << LOGPF) / 32; k += blockDim.x) dsm[k] = 0u;
+                    __syncthreads();
                     for (uint32_t k = tid; k < qlen; k += blockDim.x) {
                         const uint32_t v = q[k];
                         nq[k] = v;
                         atomicOr(nw + (v >> 5), 1u << (v & 31));
+                        const uint32_t b = pf_hash(v);
+                        atomicOr(&dsm[b >> 5], 1u << (b & 31));
                     }
                     __syncthreads();
                     q = nq;
@@ -1218,7 +1303,7 @@ uint32_t long_row_min() {  // IMMX_LONG_MIN=d: rows of degree >= d take the long
         const long v = std::atol(e);
         return v <= 0 ? 0xffffffffu : (uint32_t)v;
     }
-    return 0xffffffffu;  // off by default until it measures faster
+    return IMMX_LONG_MIN_DEFAULT;
 }
 
 bool exact_coins_forced() {  // IMMX_EXACT_COINS=1: tests drive every coin through the tie path
