@@ -227,6 +227,7 @@ struct SampCtl {
     unsigned long long edges_abandoned;  // scanned by samples that moved to the next tier
     unsigned long long n_promoted;       // samples that continued in a promotion slot
     unsigned long long probes;           // LT: cumulative-weight entries read
+    unsigned long long long_edges;       // edges of the rows that took the long-row path
 };
 
 struct SampJob {
@@ -474,6 +475,7 @@ struct BlkSmem {
     uint32_t nextrow[2][NW];  // rows of the next group's warp starts (double-buffered)
     uint32_t hdup;            // hash tiers: duplicate keys left by conflict rollbacks
     uint32_t wlong[NW];       // per warp: first long row of the batch (NB: none)
+    uint32_t lw[2][NW];       // long rows: per warp, candidates | previous slab's successes << 16
     int pslot;                // hash tiers: the promotion slot taken (-1: none)
     uint32_t lbuf[2 * NW * 32 * U];  // rare path: success positions (lbuf[0, G)) and targets (lbuf[G, 2G))
     uint32_t cut;
@@ -505,6 +507,21 @@ __device__ __forceinline__ uint32_t advance_row(const uint32_t* cum, uint32_t r,
         else lo = mid + 1;
     }
     return lo;
+}
+
+// position of the r-th (0-based) set bit of x (popc(x) > r)
+__device__ __forceinline__ uint32_t nth_bit(uint32_t x, uint32_t r) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (int w = 16; w; w >>= 1) {
+        const uint32_t c = __popc(x & ((1u << w) - 1u));
+        if (r >= c) {
+            r -= c;
+            x >>= w;
+            pos += w;
+        }
+    }
+    return pos;
 }
 
 // sum of the first `w` entries and of all NW entries of a per-warp smem array
@@ -584,7 +601,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
             sh.hdup = 0;
         }
         uint32_t qhead = 0, qlen = 1;
-        uint64_t edges = 0;
+        uint64_t edges = 0, long_edges = 0;
         bool overflow = false;
         __syncthreads();
         bool want_promote = false, no_slot = false;
@@ -629,16 +646,19 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
             // row needs no conflict check, no re-probe and no row mapping.  A slab gives thread
             // `tid` the LR consecutive positions [tid*LR, tid*LR + LR) (from the row start
             // rounded down to 16 bytes; 128-bit loads), tested against the visited set into a
-            // candidate mask; a warp scan and one CTA prefix of the candidate counts number the
-            // draws, and the lane runs its coins in position order on the running pre-mix value
-            // z = s0 + t*gamma (one 64-bit add per candidate instead of a multiply).  Successes
-            // (~1 per weighted-cascade row) reload their target and are appended in position
-            // order after a second prefix.  Two barriers per slab of NW*32*LR positions.
+            // candidate mask.  The targets of the next slab are loaded right after the tests, so
+            // they arrive while this slab's coins run.  A warp scan and one CTA prefix of the
+            // candidate counts number the draws: the lane's candidates take consecutive draws,
+            // so its coins run by rank on z = s0 + t*gamma stepped by gamma (no per-position
+            // candidate test), and the rare successes are mapped back to positions.  Successes
+            // are committed one slab late: their counts ride on the next slab's prefix, so a
+            // slab costs one barrier (plus two per row).  Targets of successes are re-read.
             auto long_row = [&](uint32_t u) {
                 const uint64_t rb = g.row[u];
                 const uint64_t D = g.row[u + 1] - rb;
                 const uint64_t Trow = PM == kProbRow ? g.thr[u] : g.gthr;
                 edges += D;
+                long_edges += D;
                 if (PM == kProbRow && Trow == kThrNever) return;  // p <= 0: no draw (sampler.cpp:38)
                 const bool always = PM == kProbRow && Trow == kThrAlways;  // p >= 1: no draw, all join
                 const uint32_t thi = (uint32_t)(Trow >> 32);
@@ -646,46 +666,55 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                 const uint32_t* __restrict__ cb = g.col + (rb - head);
                 const uint64_t span = D + head;
                 constexpr uint32_t SLAB = NW * 32 * LR;
-                for (uint64_t sb = 0; sb < span; sb += SLAB) {
-                    const uint64_t e0 = sb + (uint64_t)tid * LR;  // this thread's first element
-                    uint32_t cm = 0;                              // candidates (bit k: element e0 + k)
-                    if (e0 < span) {
-                        uint32_t v[LR];
-                        uint32_t valid;
-                        if (e0 >= head && e0 + LR <= span) {
-                            const uint4* p4 = reinterpret_cast<const uint4*>(cb + e0);
+                const uint32_t nslab = (uint32_t)((span + SLAB - 1) / SLAB);
+                uint32_t v[LR];
+                uint32_t valid = 0;
+                auto load = [&](uint64_t e0) {  // this thread's chunk of targets
+                    if (e0 >= head && e0 + LR <= span) {
+                        const uint4* p4 = reinterpret_cast<const uint4*>(cb + e0);
     #pragma unroll
-                            for (int k = 0; k < (int)LR / 4; ++k) {
-                                const uint4 x = __ldg(p4 + k);
-                                v[4 * k] = x.x;
-                                v[4 * k + 1] = x.y;
-                                v[4 * k + 2] = x.z;
-                                v[4 * k + 3] = x.w;
-                            }
-                            valid = (uint32_t)((1ull << LR) - 1);
-                        } else {
-                            valid = 0;
+                        for (int k = 0; k < (int)LR / 4; ++k) {
+                            const uint4 x = __ldg(p4 + k);
+                            v[4 * k] = x.x;
+                            v[4 * k + 1] = x.y;
+                            v[4 * k + 2] = x.z;
+                            v[4 * k + 3] = x.w;
+                        }
+                        valid = (uint32_t)((1ull << LR) - 1);
+                    } else {
+                        valid = 0;
     #pragma unroll
-                            for (int k = 0; k < (int)LR; ++k) {
-                                const bool ok = e0 + k >= head && e0 + k < span;
-                                v[k] = ok ? __ldg(cb + e0 + k) : 0u;
-                                valid |= (uint32_t)ok << k;
+                        for (int k = 0; k < (int)LR; ++k) {
+                            const bool ok = e0 + k >= head && e0 + k < span;
+                            v[k] = ok ? __ldg(cb + e0 + k) : 0u;
+                            valid |= (uint32_t)ok << k;
+                        }
+                    }
+                };
+                load((uint64_t)tid * LR);
+                uint32_t sm_prev = 0;   // successes of the previous slab (bit k: element e0_prev + k)
+                uint64_t e0_prev = 0;
+                for (uint32_t s = 0; s <= nslab; ++s) {
+                    const uint64_t e0 = (uint64_t)s * SLAB + (uint64_t)tid * LR;
+                    uint32_t cm = 0;  // candidates (bit k: element e0 + k)
+                    if (s < nslab) {
+                        if (e0 < span) {
+                            // first step, branch-free: a filter bit (hash tiers, promoted samples)
+                            // or the exact bit (bitmap tiers); the rare maybes re-read their target
+                            uint32_t fm = 0;
+    #pragma unroll
+                            for (int k = 0; k < (int)LR; ++k) fm |= (uint32_t)lmaybe(v[k]) << k;
+                            fm &= valid;
+                            cm = valid & ~fm;
+                            if constexpr (kTwoStep) {
+                                while (fm) {
+                                    const uint32_t k = __ffs(fm) - 1;
+                                    fm &= fm - 1;
+                                    if (!lexact(__ldg(cb + e0 + k))) cm |= 1u << k;
+                                }
                             }
                         }
-                        // first step, branch-free: a filter bit (hash tiers, promoted samples) or
-                        // the exact bit (bitmap tiers); the rare maybes re-read their target
-                        uint32_t fm = 0;
-    #pragma unroll
-                        for (int k = 0; k < (int)LR; ++k) fm |= (uint32_t)lmaybe(v[k]) << k;
-                        fm &= valid;
-                        cm = valid & ~fm;
-                        if constexpr (kTwoStep) {
-                            while (fm) {
-                                const uint32_t k = __ffs(fm) - 1;
-                                fm &= fm - 1;
-                                if (!lexact(__ldg(cb + e0 + k))) cm |= 1u << k;
-                            }
-                        }
+                        if (s + 1 < nslab && e0 + SLAB < span) load(e0 + SLAB);  // in flight during the coins
                     }
                     const uint32_t nc = __popc(cm);
                     uint32_t incl = nc;
@@ -694,63 +723,76 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                         const uint32_t y = __shfl_up_sync(FULL, incl, o);
                         if (lane >= (uint32_t)o) incl += y;
                     }
-                    if (lane == 31) sh.wsum[w] = incl;
+                    const uint32_t ns_prev = __popc(sm_prev);
+                    const uint32_t sw_prev = __reduce_add_sync(FULL, ns_prev);
+                    // candidates of this slab (<= 32*LR) | successes of the previous one, per warp
+                    if (lane == 31) sh.lw[s & 1][w] = incl | (sw_prev << 16);
                     __syncthreads();
-                    uint32_t cbefore, ctotal;
-                    warp_prefix<NW>(sh.wsum, w, cbefore, ctotal);
+                    uint32_t before, total;
+                    warp_prefix<NW>(sh.lw[s & 1], w, before, total);
+                    const uint32_t sbefore = before >> 16, stotal = total >> 16;
+                    // ---- commit the previous slab's successes (position order) ----
+                    if (stotal) {
+                        if (qlen + (P ? 0u : sh.hdup) + stotal > qcap) {  // CTA-uniform
+                            overflow = true;
+                            break;
+                        }
+                        if (sw_prev) {  // (warp-uniform)
+                            uint32_t sincl = ns_prev;
+    #pragma unroll
+                            for (int o = 1; o < 32; o <<= 1) {
+                                const uint32_t y = __shfl_up_sync(FULL, sincl, o);
+                                if (lane >= (uint32_t)o) sincl += y;
+                            }
+                            uint32_t pos = qlen + sbefore + sincl - ns_prev;
+                            while (sm_prev) {
+                                const uint32_t k = __ffs(sm_prev) - 1;
+                                sm_prev &= sm_prev - 1;
+                                const uint32_t x = __ldg(cb + e0_prev + k);
+                                q[pos++] = x;
+                                vadd(x);
+                            }
+                        }
+                        qlen += stotal;
+                    }
+                    // ---- this slab's coins ----
+                    const uint32_t cbefore = before & 0xffffu, ctotal = total & 0xffffu;
                     uint32_t sm = 0;
                     if (always) {
                         sm = cm;
-                    } else if (cm) {
-                        const uint64_t d0 = t + cbefore + (incl - nc);  // draw number of the first candidate
-                        uint64_t z = s0 + d0 * kGamma;
+                    } else if (nc) {
+                        // the lane's candidates take draws d0, d0+1, ...: coins by rank r
+                        const uint64_t d0 = t + cbefore + (incl - nc);
+                        const uint64_t z0 = s0 + d0 * kGamma;
+                        uint32_t sr = 0;
                         bool tie = job.exact_coins;
+                        const uint32_t nmax = __reduce_max_sync(__activemask(), nc);
+                        for (uint32_t r0 = 0; r0 < nmax; r0 += 4) {
+                            uint64_t z = z0 + (uint64_t)r0 * kGamma;
     #pragma unroll
-                        for (int k = 0; k < (int)LR; ++k) {
-                            const bool c = (cm >> k) & 1u;
-                            const uint32_t zh = zhi_of(z);
-                            sm |= (uint32_t)(c && zh < thi) << k;
-                            tie |= c && (uint32_t)(zh - thi + 1u) < 3u;  // zh in {thi - 1, thi, thi + 1}
-                            z += c ? kGamma : 0ull;
-                        }
-                        if (tie) {  // rare (~2^-31 a draw): this lane's coins on the full words
-                            sm = 0;
-                            z = s0 + d0 * kGamma;
-                            for (uint32_t k = 0; k < LR; ++k) {
-                                if (!((cm >> k) & 1u)) continue;
-                                sm |= (uint32_t)success_of(z, Trow) << k;
+                            for (uint32_t r = 0; r < 4; ++r) {
+                                const uint32_t zh = zhi_of(z);
+                                sr |= (uint32_t)(zh < thi) << (r0 + r);
+                                tie |= (uint32_t)(zh - thi + 1u) < 3u;  // zh in {thi - 1, thi, thi + 1}
                                 z += kGamma;
                             }
                         }
-                    }
-                    const uint32_t ns = __popc(sm);
-                    const uint32_t sw = __reduce_add_sync(FULL, ns);
-                    if (lane == 0) sh.wsum2[w] = sw;
-                    __syncthreads();
-                    uint32_t sbefore, stotal;
-                    warp_prefix<NW>(sh.wsum2, w, sbefore, stotal);
-                    if (qlen + (P ? 0u : sh.hdup) + stotal > qcap) {  // CTA-uniform
-                        overflow = true;
-                        break;
-                    }
-                    if (sw) {  // (warp-uniform, rare)
-                        uint32_t sincl = ns;
-    #pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const uint32_t y = __shfl_up_sync(FULL, sincl, o);
-                            if (lane >= (uint32_t)o) sincl += y;
+                        sr &= nc >= 32 ? FULL : ((1u << nc) - 1u);
+                        if (tie) {  // rare (~2^-31 a draw): this lane's coins on the full words
+                            sr = 0;
+                            uint64_t z = z0;
+                            for (uint32_t r = 0; r < nc; ++r, z += kGamma) sr |= (uint32_t)success_of(z, Trow) << r;
                         }
-                        uint32_t pos = qlen + sbefore + sincl - ns;
-                        while (sm) {
-                            const uint32_t k = __ffs(sm) - 1;
-                            sm &= sm - 1;
-                            const uint32_t x = __ldg(cb + e0 + k);
-                            q[pos++] = x;
-                            vadd(x);
+                        // rank -> position (rare)
+                        while (sr) {
+                            const uint32_t r = __ffs(sr) - 1;
+                            sr &= sr - 1;
+                            sm |= 1u << nth_bit(cm, r);
                         }
                     }
-                    qlen += stotal;
                     if (!always) t += ctotal;
+                    sm_prev = sm;
+                    e0_prev = e0;
                 }
                 __syncthreads();  // inserts and queue writes visible to the next row
             };
@@ -1162,6 +1204,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     if (job.next_draw) job.next_draw[j] = t;
                     atomicAdd(&job.ctl->edges, (unsigned long long)edges);
                     atomicAdd(&job.ctl->members, (unsigned long long)qlen);
+                    if (long_edges) atomicAdd(&job.ctl->long_edges, (unsigned long long)long_edges);
                 }
             }
         } else if (tid == 0) {
@@ -1533,9 +1576,10 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
         members += hctl->members;
         const uint32_t n_ovf = hctl->n_ovf, n_nospace = hctl->n_nospace;
         if (debug_tiers())
-            std::fprintf(stderr, "[immx sampler] tier %d%s grid %u items %u ovf %u nospace %u members %llu edges %llu abandoned %llu promoted %llu %.3f ms\n",
+            std::fprintf(stderr, "[immx sampler] tier %d%s grid %u items %u ovf %u nospace %u members %llu edges %llu (long rows %llu) abandoned %llu promoted %llu %.3f ms\n",
                          tier.kind, tier.block ? "b" : "w", warps, nitems, n_ovf, n_nospace,
                          (unsigned long long)hctl->members, (unsigned long long)hctl->edges,
+                         (unsigned long long)hctl->long_edges,
                          (unsigned long long)hctl->edges_abandoned, (unsigned long long)hctl->n_promoted,
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_launch).count());
         {
