@@ -38,6 +38,9 @@
 #ifndef IMMX_LONG_MIN_DEFAULT
 #define IMMX_LONG_MIN_DEFAULT 4096  // rows of at least this degree take the long-row path
 #endif
+#ifndef IMMX_COIN_FMA
+#define IMMX_COIN_FMA 0  // 1: one 64-bit shift of the long-row coins on the multiply-add pipe (measured: no gain)
+#endif
 #ifndef IMMX_LONG_LR
 #define IMMX_LONG_LR 16  // positions per thread per long-row slab (multiple of 4, <= 32)
 #endif
@@ -90,6 +93,35 @@ __device__ __forceinline__ uint32_t zhi_of(uint64_t z) {
     return __umulhi(ylo, 0x133111ebu) + ylo * 0x94d049bbu + yhi * 0x133111ebu;
 }
 __device__ __forceinline__ bool success_of(uint64_t z, uint64_t tsh) { return coin_success(z, 0, tsh); }
+// zdiff_of with splitmix64's first shift (z >> 30) done as multiplies by k4 = 4 (the caller
+// passes it through memory so the compiler keeps the multiplies): the integer-ALU pipe is the
+// sampler's busiest, the multiply-add pipe has room
+__device__ __forceinline__ uint32_t mulhi_u32(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t madhi_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t zdiff_fma(uint64_t z, uint32_t a, uint32_t k4) {
+    const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+    const uint32_t slo = madhi_u32(lo, k4, hi * k4);  // (lo >> 30) | (hi << 2)
+    const uint32_t shi = mulhi_u32(hi, k4);           // hi >> 30
+    z = ((uint64_t)(hi ^ shi) << 32 | (lo ^ slo)) * 0xbf58476d1ce4e5b9ULL;
+    const uint64_t y = z ^ (z >> 27);
+    const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
+    return __umulhi(ylo, 0x133111ebu) + ylo * 0x94d049bbu + (yhi * 0x133111ebu + a);
+}
+// zhi_of(z) + a (mod 2^32), the addend folded into the last multiply-add
+__device__ __forceinline__ uint32_t zdiff_of(uint64_t z, uint32_t a) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    const uint64_t y = z ^ (z >> 27);
+    const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
+    return __umulhi(ylo, 0x133111ebu) + ylo * 0x94d049bbu + (yhi * 0x133111ebu + a);
+}
 
 // High word of the draw before splitmix64's last step (x = z ^ (z >> 31)), zhi.  The last step
 // flips bit 0 of the high word when bit 31 is set, so x < (T << 11) agrees with zhi < thi (thi
@@ -252,6 +284,8 @@ struct SampJob {
     int model;
     int exact_coins;                 // test knob: every coin through the exact (tie) path
     uint32_t long_min;               // rows of at least this degree run the long-row path
+    uint32_t k4;                     // = 4: a multiplier the compiler cannot see (keeps a shift on the
+                                     // multiply-add pipe, zdiff_fma)
                                      // (0xffffffff: never -- per-edge p, multigraph rows, LT)
     unsigned int* run_hist;          // non-null: the pool's running vertex histogram (select_raw's),
                                      // counted as the sets are committed
@@ -761,22 +795,29 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     if (always) {
                         sm = cm;
                     } else if (nc) {
-                        // the lane's candidates take draws d0, d0+1, ...: coins by rank r
+                        // the lane's candidates take draws d0, d0+1, ...: coins by rank r.  Per draw
+                        // e = zh - thi + 1 comes out of the last multiply-add; e < 3 flags a tie
+                        // (zh in {thi - 1, thi, thi + 1}), otherwise zh < thi <=> e >= 1 - thi
+                        // (mod 2^32; needs thi >= 2 -- smaller thresholds take the exact path)
                         const uint64_t d0 = t + cbefore + (incl - nc);
                         const uint64_t z0 = s0 + d0 * kGamma;
-                        uint32_t sr = 0;
-                        bool tie = job.exact_coins;
+                        const uint32_t nt = 1u - thi;
+                        const uint32_t k4 = job.k4;
+                        uint32_t sr = 0, emin = (thi < 2u || job.exact_coins) ? 0u : FULL;
                         const uint32_t nmax = __reduce_max_sync(__activemask(), nc);
-                        for (uint32_t r0 = 0; r0 < nmax; r0 += 4) {
-                            uint64_t z = z0 + (uint64_t)r0 * kGamma;
+                        uint64_t z = z0;
+    #pragma unroll
+                        for (uint32_t r0 = 0; r0 < LR; r0 += 4) {
+                            if (r0 >= nmax) break;  // (warp-uniform)
     #pragma unroll
                             for (uint32_t r = 0; r < 4; ++r) {
-                                const uint32_t zh = zhi_of(z);
-                                sr |= (uint32_t)(zh < thi) << (r0 + r);
-                                tie |= (uint32_t)(zh - thi + 1u) < 3u;  // zh in {thi - 1, thi, thi + 1}
+                                const uint32_t e = IMMX_COIN_FMA ? zdiff_fma(z, nt, k4) : zdiff_of(z, nt);
+                                if (e >= nt) sr |= 1u << (r0 + r);
+                                emin = min(emin, e);
                                 z += kGamma;
                             }
                         }
+                        const bool tie = emin < 3u;
                         sr &= nc >= 32 ? FULL : ((1u << nc) - 1u);
                         if (tie) {  // rare (~2^-31 a draw): this lane's coins on the full words
                             sr = 0;
@@ -1502,6 +1543,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     job.ctl = ctl.p;
     job.model = model;
     job.exact_coins = exact_coins_forced() ? 1 : 0;
+    job.k4 = 4;
     job.long_min = long_row_min();
     if (G.row_dups || gv.pmode == kProbEdge || model != IMMX_MODEL_IC) job.long_min = 0xffffffffu;
     // select_raw's running histogram of this pool, when it already covers exactly the sets
