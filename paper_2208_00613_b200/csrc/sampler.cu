@@ -41,6 +41,9 @@
 #ifndef IMMX_COIN_FMA
 #define IMMX_COIN_FMA 0  // 1: one 64-bit shift of the long-row coins on the multiply-add pipe (measured: no gain)
 #endif
+#ifndef IMMX_LONG_BITMAP
+#define IMMX_LONG_BITMAP 0  // 1: the long-row path in the bitmap tiers too (c2: 243 -> 226 Gedges/s)
+#endif
 #ifndef IMMX_LONG_LR
 #define IMMX_LONG_LR 16  // positions per thread per long-row slab (multiple of 4, <= 32)
 #endif
@@ -580,6 +583,9 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
     constexpr bool kHash = KIND == kBHash13 || KIND == kBHash15;
     // positions per thread per long-row slab
     constexpr uint32_t LR = IMMX_LONG_LR;
+    // the long-row path in this instantiation (IMMX_LONG_BITMAP=0: not in the bitmap tiers of
+    // small graphs)
+    constexpr bool kLongPath = IMMX_LONG_BITMAP || !(KIND == kBBits || KIND == kBBitsS);
     // a promoted sample's filter: one bit per vertex hash over the idle hash slots (2^(LOGH+5) bits)
     constexpr uint32_t LOGPF = (KIND == kBHash15 ? 15 : 13) + 5;
     auto pf_hash = [](uint32_t v) -> uint32_t { return (v * 0x2C1B3C6Du) >> (32 - LOGPF); };
@@ -858,7 +864,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                     deg = (uint32_t)(g.row[u + 1] - rs);
                     if (PM == kProbRow) th = g.thr[u];
                 }
-                if constexpr (PM != kProbEdge) {
+                if constexpr (PM != kProbEdge && kLongPath) {
                     if (job.long_min != 0xffffffffu) {  // the batch ends before its first long row
                         const uint32_t lb = __ballot_sync(FULL, tid < nb && deg >= job.long_min);
                         if (lane == 0) sh.wlong[w] = lb ? w * 32 + __ffs(lb) - 1 : NB;

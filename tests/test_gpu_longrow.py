@@ -41,13 +41,15 @@ def test_long_rows_rmat_bitmap_tier(im, orc, long_min):
     assert b[2]["edges"] == a[2]
 
 
-@pytest.mark.parametrize("p", [0.006, 0.1])
+@pytest.mark.parametrize("p", [0.006, 0.1, 1.0, 0.0])
 def test_long_rows_hash_promotion_and_global_tiers(im, orc, long_min, p):
-    # n = 2^20: hash tier, promotion slots (p = 0.006) and sets beyond a slot (p = 0.1)
+    # n = 2^20: hash tier, promotion slots (p = 0.006), sets beyond a slot (p = 0.1), rows that
+    # join without a draw (p = 1) and rows that never draw (p = 0).  (The long-row path is
+    # compiled for these tiers only: the bitmap tiers of small graphs run the general path.)
     g = im.generate_rmat(20, 8, 0.57, 0.19, 0.19, 11)
     im.assign_weights_f32(g, "uniform", p)
     gt = orc.transpose(csr_of(g))
-    cnt = 300 if p < 0.05 else 24
+    cnt = 300 if p < 0.05 else (24 if p < 1.0 else 6)
     a = orc.sample_block(gt, cnt, 0, 5)
     b = sample_dev(im, gt, cnt, 0, 5)
     assert_same_sets(a[0], a[1], b[0], b[1])

@@ -36,15 +36,19 @@ def main():
         g = bench.make_graph(im, cfg)
         print(f"graph {g} in {time.time() - t:.1f}s", flush=True)
         dg = im.DeviceGraph(g, transposed=False, device=dev)
-    print("prob mode", dg.prob_mode, flush=True)
+    model = 0
+    if "lt_seed" in cfg:  # c3: LT walks (weights generated in HBM)
+        dg.set_lt_random(cfg["lt_seed"])
+        model = 1
+    print("prob mode", dg.prob_mode, "model", "LT" if model else "IC", flush=True)
     for rep in range(a.reps):
         pool = im.Pool(dev)
-        pool.sample(dg, 2048, a.first, 42)  # pilot: sizes the arena, so the measured batch is one launch
+        pool.sample(dg, 2048, a.first, 42, model)  # pilot: sizes the arena, so the measured batch is one launch
         dev.synchronize()
         dev.profile(True)
         dev.reset_stats()
         t = time.time()
-        pool.sample(dg, a.count, a.first + 2048, 42)
+        pool.sample(dg, a.count, a.first + 2048, 42, model)
         dev.synchronize()
         wall = time.time() - t
         st = dev.kernel_stats("sample")
