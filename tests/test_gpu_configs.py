@@ -70,8 +70,10 @@ def config_run(im, name):
         gd = golden(name)
         cfg = CONFIGS[name]
         dg = device_graph(im, cfg)
+        # the golden's worker count: the reference's selection ledger (per-worker frequency
+        # tables and decode buffers, select.cpp:75-79, :218-223) depends on it
         r = im.run_device(dg, cfg["k"], epsilon=cfg["eps"], blocks=cfg["blocks"], mode=cfg["mode"], seed=42,
-                          keep=True)
+                          workers=gd["workers"], keep=True)
         _CACHE[name] = (gd, dg, r)
     return _CACHE[name]
 
