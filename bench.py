@@ -74,6 +74,112 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+class NvmlClockSampler:
+    """SM clock + clock-event (throttle) reasons polled through NVML in a thread of this
+    process during the timed region.  (An `nvidia-smi -lms` child stalled the driver for tens
+    of ms per query -- c2 +60..140 ms a step; NVML's two queries do not.)"""
+
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap")]
+
+    def __init__(self, gpu: int, period_ms: int = 200):
+        import pynvml as N
+
+        self.N, self.rows, self.period_ms, self.late = N, [], period_ms, False
+        N.nvmlInit()
+        self.h = None
+        try:  # the CUDA device's NVML handle (indices differ under CUDA_VISIBLE_DEVICES)
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(gpu).uuid)
+            self.h = N.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            self.h = N.nvmlDeviceGetHandleByIndex(gpu)
+        self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+        self.stop = threading.Event()
+
+    def _poll(self):
+        N = self.N
+        while not self.stop.is_set():
+            try:
+                mhz = float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((mhz, rs))
+            except Exception:
+                pass
+            self.stop.wait(self.period_ms / 1000.0)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
+        return self
+
+    def wait_first(self, timeout: float = 10.0):
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.01)
+        self.rows.clear()
+
+    def ensure_one(self):
+        self.late = not self.rows
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < self.period_ms / 1000.0 + 1.0:
+            time.sleep(0.01)
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        N = self.N
+        reasons = sorted({name for _, rs in self.rows for name, attr in self.REASONS
+                          if hasattr(N, attr) and rs & getattr(N, attr)})
+        out = {"sm_mhz": float(np.median([m for m, _ in self.rows])), "sm_max_mhz": self.max_mhz,
+               "reasons": reasons, "samples": len(self.rows), "period_ms": self.period_ms, "source": "nvml"}
+        if self.late:
+            out["sampled"] = "right after the timed region (shorter than the sampling period)"
+        return out
+
+
+class NoClockSampler:
+    """BENCH_CLOCKS=off: no queries at all (diagnosis of the samplers' own cost only -- a line
+    without clocks does not meet the bench contract)."""
+
+    rows, late = [], False
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+    def wait_first(self, timeout: float = 10.0):
+        pass
+
+    def ensure_one(self):
+        pass
+
+    def summary(self):
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled (BENCH_CLOCKS=off)"], "samples": 0}
+
+
+def clock_sampler(gpu: int, period_ms: int):
+    """NVML in-process when available (BENCH_CLOCKS=smi forces the nvidia-smi child)."""
+    mode = os.environ.get("BENCH_CLOCKS", "nvml")
+    if mode == "off":
+        return NoClockSampler()
+    if mode != "smi":
+        try:
+            return NvmlClockSampler(gpu, period_ms)
+        except Exception:
+            pass
+    return ClockSampler(gpu, period_ms)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
 
@@ -324,12 +430,10 @@ def run_ours(args, cfg, rank, world, local):
     for _ in range(args.warmup):
         one_step()
     dev.synchronize()
-    # each nvidia-smi query can stall the driver for tens of ms (measured: 29 queries at 200 ms
-    # cost config 2 +140 ms a step on one box), which distorts the timed region: regions
-    # expected under 2 s are sampled every 2 s -- in practice right after the region --, longer
-    # ones once a second (5+ samples inside config 2's region)
+    # NVML polling every 250 ms (the nvidia-smi fallback: each of its queries could stall the
+    # driver for tens of ms, so it samples once a second in regions >= 2 s, else right after)
     expect_s = (time.perf_counter() - tw) / max(args.warmup, 1) * args.steps
-    period_ms = 1000 if expect_s >= 2.0 else 2000
+    period_ms = int(os.environ.get("BENCH_CLOCK_MS", "0")) or (1000 if expect_s >= 2.0 else 2000)
 
     # ---- timed: graph resident in HBM ----
     dev.profile(True)
@@ -340,15 +444,19 @@ def run_ours(args, cfg, rank, world, local):
     dev.synchronize()
     samples = 0
     results = []
-    with ClockSampler(local, period_ms) as clk:
+    with clock_sampler(local, period_ms) as clk:
         clk.wait_first()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             ev0.record(stream)
+        marks = []
         for _ in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.fill_(1)  # L2 flush between steps, on the library stream
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                marks.append(e)
             r = one_step()
             samples += r["samples_drawn"]
             results.append(r)
@@ -360,6 +468,8 @@ def run_ours(args, cfg, rank, world, local):
     torch.cuda.synchronize()
     barrier(world)
     ms_local = ev0.elapsed_time(ev1)
+    # per step: from the end of its L2 flush to the next step's (or the region's end)
+    step_ms = [marks[i].elapsed_time(marks[i + 1] if i + 1 < len(marks) else ev1) for i in range(len(marks))]
     launches = dev.kernel_launches - launches0
     samp = dev.kernel_stats("sample")
     hsel = dev.kernel_stats("hselect")
@@ -438,6 +548,7 @@ def run_ours(args, cfg, rank, world, local):
         "config": config_dict(args, cfg, world),
         "theta": r0["theta"], "reuse_pool": True,
         "imm_end_to_end_s": ms / args.steps / 1000.0,
+        "step_ms": [round(x, 2) for x in step_ms],
         "compression_ratio": r0["compression_ratio"],
         "dense_sets": r0.get("dense_sets", 0),
         "compression_ratio_device": r0["raw_bytes"] / r0["device_store_bytes"] if r0["device_store_bytes"] else None,

@@ -365,6 +365,25 @@ int immx_device_create(int ordinal, immx_device** out) {
         CK(cudaDeviceGetDefaultMemPool(&mp, ordinal));
         uint64_t keep_all = ~0ULL;  // keep freed memory in the pool for the next run
         CK(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep_all));
+        // Pre-map one large block into the pool and free it: later allocations are carved out
+        // of it, so a run never waits on the driver mapping fresh memory (measured: c2's
+        // selection setup took 0.1..231 ms depending on whether the pool had to grow).
+        // IMMX_POOL_RESERVE_GB (default: half the free memory, at most 96 GB; 0 disables).
+        {
+            size_t fr = 0, tot = 0;
+            CK(cudaMemGetInfo(&fr, &tot));
+            uint64_t want = std::min<uint64_t>(fr / 2, 96ULL << 30);
+            if (const char* e = std::getenv("IMMX_POOL_RESERVE_GB")) want = std::min<uint64_t>(fr / 2, (uint64_t)std::atof(e) * (1ULL << 30));
+            if (want >= (1ULL << 30)) {
+                void* p = nullptr;
+                if (cudaMallocAsync(&p, want, d.stream) == cudaSuccess) {
+                    CK(cudaFreeAsync(p, d.stream));
+                    CK(cudaStreamSynchronize(d.stream));
+                } else {
+                    cudaGetLastError();
+                }
+            }
+        }
         d.scal.exact(64);
         CK(cudaMallocHost(&d.host_scal, 64 * 8));
         admit.ok = true;

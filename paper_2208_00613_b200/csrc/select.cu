@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <memory>
@@ -688,6 +689,17 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
     const uint64_t theta = S.count, n = S.n;
     if (theta == 0) fail(IMMX_EINVAL, "selection requires at least one set");
     if (k >= n) fail(IMMX_EINVAL, "selection requires k < n");
+    const auto tq0 = std::chrono::steady_clock::now();
+    static const bool dbg_phases = [] {
+        const char* e = std::getenv("IMMX_DEBUG_PHASES");
+        return e && *e && *e != '0';
+    }();
+    auto tq = [&](const char* what) {
+        if (!dbg_phases) return;
+        CK(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[immx select] %s at %.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0).count());
+    };
     DBuf<uint32_t> deleted;  // 0: live; r+1: covered in round r
     DBuf<uint8_t> is_seed;
     deleted.exact(theta);
@@ -733,6 +745,7 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
     DBuf<unsigned int> hist_b;  // the second table (recount target, double-buffered)
     hist_b.exact(n);
     const unsigned grid_am = grid_for(n, d);
+    tq("setup");
     std::vector<KTimer> kt(k);
     for (uint32_t r = 0; r < k; ++r) {
         k_argmax_pick<<<grid_am, 256, 0, s>>>(d_hist, hist_b.p, n, ctl, keys.p, r, is_seed.p, seeds.p, marg.p);
@@ -761,6 +774,7 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
         CK_LAUNCH("select_huffman round");
         d.kernel_launches += 3 + (nd ? 2 : 0);
     }
+    tq("rounds");
     std::vector<unsigned long long> hbytes(k);
     CK(cudaMemcpyAsync(hbytes.data(), rbytes.p, k * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
