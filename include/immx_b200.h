@@ -141,6 +141,13 @@ IMMX_API int immx_device_reset_stats(immx_device* d);
  * (weighted cascade, uniform) are stored per row / once. */
 IMMX_API int immx_graph_upload(immx_device* d, uint64_t n, uint64_t m, const uint64_t* offsets,
                       const uint32_t* targets, const double* probs, int transposed, immx_graph** out);
+/* The same with the probabilities given by a weight model instead of per edge -- the
+ * reference's assign_weights (graph.cpp:146-157) applied on the device, with float32 values
+ * (BASELINE's configs): weight_model 0 = weighted cascade fl32(1/indeg(v)), 1 = uniform
+ * fl32(p).  Only the CSR crosses PCIe (8(n+1) + 4m bytes instead of + 8m of probabilities). */
+IMMX_API int immx_graph_upload_model(immx_device* d, uint64_t n, uint64_t m, const uint64_t* offsets,
+                                     const uint32_t* targets, int weight_model, double p, int transposed,
+                                     immx_graph** out);
 /* Synthetic R-MAT generated directly in HBM as the reverse CSR -- the same graph as
  * immx_hgraph_generate_rmat + transpose (bit-identical), without host memory or a transpose.
  * weight_model 0 = weighted cascade fl32(1/indeg(v)), 1 = uniform fl32(p). */

@@ -245,13 +245,19 @@ class DeviceGraph:
             check(lib.immx_graph_set_lt_weights(self.h, ptr(w, C.c_float)))
 
     @classmethod
-    def from_arrays(cls, n, off, tgt, pr, transposed, device=None):
+    def from_arrays(cls, n, off, tgt, pr, transposed, device=None, weights=None, p=0.1):
+        """CSR arrays (host) -> HBM.  pr: f64 per edge; or pr=None with weights="wc" / "uniform"
+        (assign_weights with float32 values, applied on the device: only the CSR is copied)."""
         self = cls.__new__(cls)
         self.device = device or default_device()
         self.n, self.m = int(n), int(tgt.size)
         h = C.c_void_p()
-        check(lib.immx_graph_upload(self.device.h, self.n, self.m, ptr(off, C.c_uint64), ptr(tgt, C.c_uint32),
-                                    ptr(pr, C.c_double), int(transposed), C.byref(h)))
+        if pr is None:
+            check(lib.immx_graph_upload_model(self.device.h, self.n, self.m, ptr(off, C.c_uint64), ptr(tgt, C.c_uint32),
+                                              _weight_model(weights or "wc"), float(p), int(transposed), C.byref(h)))
+        else:
+            check(lib.immx_graph_upload(self.device.h, self.n, self.m, ptr(off, C.c_uint64), ptr(tgt, C.c_uint32),
+                                        ptr(pr, C.c_double), int(transposed), C.byref(h)))
         self.h = h
         return self
 

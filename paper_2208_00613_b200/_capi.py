@@ -103,6 +103,7 @@ SIGNATURES = {
     "immx_device_kernel_stats": (I, [P, I, pu64, pdbl, pu64]),
     "immx_device_reset_stats": (I, [P]),
     "immx_graph_upload": (I, [P, u64, u64, pu64, pu32, pdbl, I, PP]),
+    "immx_graph_upload_model": (I, [P, u64, u64, pu64, pu32, I, dbl, I, PP]),
     "immx_graph_generate_rmat": (I, [P, u32, u32, dbl, dbl, dbl, u64, I, dbl, PP]),
     "immx_graph_download": (I, [P, pu64, pu32, pdbl]),
     "immx_graph_set_lt_weights": (I, [P, pflt]),

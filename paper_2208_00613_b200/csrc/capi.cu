@@ -475,6 +475,25 @@ int immx_graph_upload(immx_device* dv, uint64_t n, uint64_t m, const uint64_t* o
         *out = g;
     });
 }
+int immx_graph_upload_model(immx_device* dv, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt,
+                            int weight_model, double p, int transposed, immx_graph** out) {
+    return guard([&] {
+        need(dv, "device");
+        need(off, "offsets");
+        need(out, "out");
+        if (m && !tgt) fail(IMMX_EINVAL, "targets are NULL");
+        if (weight_model != 0 && weight_model != 1) fail(IMMX_EINVAL, "unknown weight model");
+        if (weight_model == 1 && !(p >= 0.0 && p <= 1.0)) fail(IMMX_EINVAL, "uniform edge probability must be in [0,1]");
+        auto* g = new immx_graph;
+        try {
+            graph_upload(g->g, dv->d, n, m, off, tgt, nullptr, transposed != 0, weight_model, p);
+        } catch (...) {
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
 int immx_graph_generate_rmat(immx_device* dv, uint32_t scale, uint32_t ef, double a, double b, double c,
                              uint64_t seed, int weight_model, double p, immx_graph** out) {
     return guard([&] {

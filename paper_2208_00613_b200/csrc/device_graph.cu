@@ -46,7 +46,7 @@ __global__ void k_gather_t(const uint32_t* __restrict__ eid, const uint32_t* __r
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t e = eid[i];
         col_t[i] = src[e];
-        prob_t[i] = prob[e];
+        if (prob) prob_t[i] = prob[e];
     }
 }
 
@@ -64,10 +64,10 @@ __global__ void k_row_scan(const uint64_t* __restrict__ row, const uint32_t* __r
             if (lane == 0) rthr[v] = 0;
             continue;
         }
-        const double p0 = prob[b];
+        const double p0 = prob ? prob[b] : 0.0;
         bool mixed = false, unsorted = false;
         for (uint64_t i = b + lane; i < e; i += 32) {
-            mixed |= !(prob[i] == p0) && !(prob[i] != prob[i] && p0 != p0);
+            if (prob) mixed |= !(prob[i] == p0) && !(prob[i] != prob[i] && p0 != p0);
             if (i + 1 < e) unsorted |= !(col[i] < col[i + 1]);
         }
         const uint32_t fm = __ballot_sync(0xffffffffu, mixed), fu = __ballot_sync(0xffffffffu, unsorted);
@@ -131,6 +131,21 @@ __global__ void k_lt_random_cum(const uint64_t* __restrict__ row, uint64_t n, ui
     }
 }
 
+// assign_weights (graph.cpp:146-157) as thresholds, float32 values: model 0 = weighted cascade,
+// every Gt row v shares fl32(1 / len(row v)); model 1 = uniform p (already rounded to f32)
+__global__ void k_model_row_thr(const uint64_t* __restrict__ row, uint64_t n, int model, double p,
+                                uint64_t* __restrict__ rthr) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t len = row[v + 1] - row[v];
+        uint64_t T = 0;
+        if (len) {
+            T = prob_threshold(model == 0 ? (double)(float)(1.0 / (double)len) : p);
+            T = (T == kThrNever || T == kThrAlways) ? T : (T << 11);
+        }
+        rthr[v] = T;
+    }
+}
+
 unsigned grid_for(uint64_t items, const Device& d, unsigned per_thread = 1) {
     uint64_t b = (items / per_thread + 255) / 256;
     b = std::min<uint64_t>(b, (uint64_t)d.num_sms * 16);
@@ -140,7 +155,7 @@ unsigned grid_for(uint64_t items, const Device& d, unsigned per_thread = 1) {
 }  // namespace
 
 void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt,
-                  const double* prob, bool transposed) {
+                  const double* prob, bool transposed, int weight_model, double wp) {
     cudaStream_t s = d.stream;
     if (n == 0) fail(IMMX_EINVAL, "graph has no vertices");
     if (n >= 0xffffffffULL) fail(IMMX_EINVAL, "vertex ids are 32-bit");
@@ -151,12 +166,16 @@ void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t
     G.m = m;
     G.row.exact(n + 1);
     G.col.exact(std::max<uint64_t>(m, 1));
+    // prob == nullptr: the probabilities follow `weight_model` (assign_weights, graph.cpp:146-157,
+    // with float32 values: 0 = weighted cascade fl32(1/indeg(v)), 1 = uniform fl32(wp)) and are
+    // derived here from the reverse CSR -- nothing per edge crosses PCIe
+    const bool by_model = prob == nullptr;
     DBuf<double> dprob;
-    dprob.exact(std::max<uint64_t>(m, 1));
+    if (!by_model) dprob.exact(std::max<uint64_t>(m, 1));
     if (transposed) {
         CK(cudaMemcpyAsync(G.row.p, off, (n + 1) * 8, cudaMemcpyHostToDevice, s));
         if (m) CK(cudaMemcpyAsync(G.col.p, tgt, m * 4, cudaMemcpyHostToDevice, s));
-        if (m) CK(cudaMemcpyAsync(dprob.p, prob, m * 8, cudaMemcpyHostToDevice, s));
+        if (m && !by_model) CK(cudaMemcpyAsync(dprob.p, prob, m * 8, cudaMemcpyHostToDevice, s));
     } else {
         // device transpose (graph.cpp:125-144)
         DBuf<uint64_t> foff;
@@ -164,7 +183,7 @@ void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t
         DBuf<double> fprob;
         foff.exact(n + 1);
         ftgt.exact(std::max<uint64_t>(m, 1));
-        fprob.exact(std::max<uint64_t>(m, 1));
+        if (!by_model) fprob.exact(std::max<uint64_t>(m, 1));
         src.exact(std::max<uint64_t>(m, 1));
         eid_in.exact(std::max<uint64_t>(m, 1));
         eid_out.exact(std::max<uint64_t>(m, 1));
@@ -172,7 +191,7 @@ void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t
         CK(cudaMemcpyAsync(foff.p, off, (n + 1) * 8, cudaMemcpyHostToDevice, s));
         if (m) {
             CK(cudaMemcpyAsync(ftgt.p, tgt, m * 4, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(fprob.p, prob, m * 8, cudaMemcpyHostToDevice, s));
+            if (!by_model) CK(cudaMemcpyAsync(fprob.p, prob, m * 8, cudaMemcpyHostToDevice, s));
             k_iota_u32<<<grid_for(m, d), 256, 0, s>>>(eid_in.p, m);
             k_expand_src<<<grid_for(n * 32, d), 256, 0, s>>>(foff.p, n, src.p);
             d.kernel_launches += 2;
@@ -214,6 +233,10 @@ void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t
     CK(cudaStreamSynchronize(s));
     G.row_dups = (hflags[0] & 2u) != 0;
     G.max_deg = hflags[1];
+    if (by_model) {
+        k_model_row_thr<<<grid_for(n, d), 256, 0, s>>>(G.row.p, n, weight_model, (double)(float)wp, rthr.p);
+        d.kernel_launches++;
+    }
     if (hflags[0] & 1u) {
         G.pmode = kProbEdge;
         G.thr.exact(std::max<uint64_t>(m, 1));

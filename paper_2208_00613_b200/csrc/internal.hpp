@@ -287,7 +287,7 @@ struct SelectOut {
 
 // device_graph.cu
 void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt,
-                  const double* prob, bool transposed);
+                  const double* prob, bool transposed, int weight_model = 0, double wp = 0.0);
 void graph_set_lt(DevGraph& G, const float* w);
 void graph_set_lt_random(DevGraph& G, uint64_t seed);
 // device_gen.cu
