@@ -514,6 +514,16 @@ class Store:
         check(lib.immx_store_decode_find(self.h, j, top, C.byref(found), ptr(dec, C.c_uint32), C.byref(nd)))
         return bool(found.value), dec[: nd.value].tolist()
 
+    def encode(self, pool: "Pool", lo: int, hi: int, top=None):
+        """huffman.cpp:107-127 for sets [lo, hi) of a device pool, appended to the store."""
+        check(lib.immx_store_encode(self.h, pool.h, lo, hi, -1 if top is None else int(top)))
+
+    def append(self, bits: bytes, bit_length: int, copied=()):
+        """One EncodedRrr from host bytes (huffman.hpp:39-45), appended as is."""
+        b = np.frombuffer(bits, np.uint8).copy() if bits else np.zeros(0, np.uint8)
+        cp = arr(copied, np.uint32)
+        check(lib.immx_store_append(self.h, ptr(b, C.c_uint8), b.size, int(bit_length), ptr(cp, C.c_uint32), cp.size))
+
     def set_hybrid(self, enable: bool = True):
         """Per-set hybrid (extension): later-encoded sets above n/32 become n-bit bitmaps."""
         check(lib.immx_store_set_hybrid(self.h, int(bool(enable))))

@@ -1044,6 +1044,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     store->s.count = store->s.total_words = store->s.total_copied = store->s.payload_bytes = 0;
                     store->s.dense_count = 0;
                     store->s.n_extra = 0;
+                    store->s.sig_k = default_sig_k();
                     store->s.hybrid = mode == IMMX_MODE_HYBRID;
                     store_set_leaf_codes(store->s, d, n, cb, {}, 1);
                 } else if (mode == IMMX_MODE_BITMAP) {

@@ -42,7 +42,8 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
                            uint64_t* __restrict__ nwords, uint64_t* __restrict__ ncopied, uint8_t* __restrict__ swap,
                            unsigned long long* __restrict__ payload, uint64_t dense_n, uint64_t base,
                            uint32_t* __restrict__ dense_ids, unsigned long long* __restrict__ dense_cnt,
-                           uint32_t* __restrict__ msize, uint32_t* __restrict__ ncw, uint64_t* __restrict__ nx) {
+                           uint32_t* __restrict__ msize, uint32_t* __restrict__ ncw, uint64_t* __restrict__ nx,
+                           uint64_t* __restrict__ sig, uint32_t sig_k) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -61,6 +62,7 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
                 swap[k] = 0;
                 ncw[k] = 0;
                 nx[k] = 0;
+                if (sig) sig[k] = 0;  // never a decode candidate: the k_dense_* passes test its bitmap
                 atomicAdd(payload, (unsigned long long)(4 * nwd));
                 dense_ids[atomicAdd(dense_cnt, 1ull)] = (uint32_t)(base + k);
             }
@@ -68,16 +70,19 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
         }
         uint32_t nb = 0, nc = 0;
         bool has_top = false;
+        uint64_t sg = 0;
         for (uint32_t i = lane; i < l; i += 32) {
             const uint32_t v = arena[b + i];
             const uint32_t cl = code_len[v];
             nb += cl;
             nc += cl == 0;
             has_top |= top_coded && v == (uint32_t)top;
+            sg |= sig_mask(v, sig_k);
         }
         for (int o = 16; o; o >>= 1) {
             nb += __shfl_xor_sync(FULL, nb, o);
             nc += __shfl_xor_sync(FULL, nc, o);
+            sg |= __shfl_xor_sync(FULL, sg, o);
         }
         has_top = __any_sync(FULL, has_top);
         if (lane == 0) {
@@ -88,6 +93,7 @@ __global__ void k_enc_size(const uint32_t* __restrict__ arena, const uint64_t* _
             swap[k] = has_top;
             const uint32_t cw = l - nc;
             ncw[k] = cw;
+            if (sig) sig[k] = sg;
             nx[k] = cw > kSegCodewords ? (cw - 1) / kSegCodewords : 0;
             atomicAdd(payload, (unsigned long long)((nb + 7) / 8 + 4ull * nc));
         }
@@ -352,6 +358,7 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     S.ncw.reserve(base + cnt, s);
     S.segd.reserve(base + cnt, s);
     S.xfirst.reserve(base + cnt, s);
+    if (S.sig_k) S.sig.reserve(base + cnt, s);
     DBuf<uint64_t> nwords, ncp, nx, xoff;
     DBuf<uint8_t> swap;
     nwords.exact(cnt);
@@ -371,7 +378,8 @@ void store_encode(Store& S, const Pool& P, uint64_t lo, uint64_t hi, int64_t top
     k_enc_size<<<grid_for(cnt * 32, d), 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, lo, hi, S.code_len.p, top,
                                                    S.bits.p + base, nwords.p, ncp.p, swap.p, d_payload,
                                                    S.hybrid ? S.n : 0, base, S.dense_ids.p, d_dense,
-                                                   S.msize.p + base, S.ncw.p + base, nx.p);
+                                                   S.msize.p + base, S.ncw.p + base, nx.p,
+                                                   S.sig_k ? S.sig.p + base : nullptr, S.sig_k);
     kt_size.stop();
     CK_LAUNCH("k_enc_size");
     d.kernel_launches++;
@@ -476,6 +484,11 @@ void store_append_host(Store& S, const uint8_t* bytes, uint64_t n_bytes, uint64_
     S.ncw.reserve(base + 1, s);
     S.segd.reserve(base + 1, s);
     S.xfirst.reserve(base + 1, s);
+    if (S.sig_k) {  // members unknown without decoding: the set passes every signature test
+        S.sig.reserve(base + 1, s);
+        const uint64_t ones = ~0ull;
+        CK(cudaMemcpyAsync(S.sig.p + base, &ones, 8, cudaMemcpyHostToDevice, s));
+    }
     {
         DBuf<uint32_t> dec;
         dec.exact(bit_length + 1);

@@ -9,6 +9,18 @@ namespace immx_dev {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
+// ---- per-set member signature (a side index of the store, like the decode checkpoints) ----
+// 64 bits per set: every member sets `k` bits chosen by a multiplicative hash of its id.  A
+// selection round tests the pick's bits first: a set whose signature lacks one cannot hold
+// the pick, so the find pass decodes only the sets that pass (the hits and the signature's
+// false positives) instead of every live set.  The streams and the results are unchanged.
+__device__ __forceinline__ uint64_t sig_mask(uint32_t v, uint32_t k) {
+    const uint32_t h = v * 0x9E3779B1u;
+    uint64_t m = 1ull << (h >> 26);
+    if (k > 1) m |= 1ull << ((h >> 20) & 63u);
+    if (k > 2) m |= 1ull << ((h >> 14) & 63u);
+    return m;
+}
 
 // ---- bit reader over one set's stream -------------------------------------------
 // The word after the buffered ones is loaded one refill ahead (pf), so a refill does not

@@ -238,6 +238,13 @@ inline void pool_release(Pool& P) {
 
 // Huffman-encoded store.  Set j: words[woff[j] ..] holds its MSB-first byte stream
 // (bytes in stream order in memory), bits[j] its bit length; copied[coff[j] .. coff[j+1]).
+inline uint32_t default_sig_k() {
+    const char* e = std::getenv("IMMX_SIG_K");
+    if (!e || !*e) return 2;
+    const long v = std::strtol(e, nullptr, 10);
+    return v < 0 ? 0u : v > 3 ? 3u : (uint32_t)v;
+}
+
 struct Store {
     Device* dev = nullptr;
     uint64_t n = 0;
@@ -258,8 +265,12 @@ struct Store {
     DBuf<uint32_t> xfirst; // count: index of the set's first extra segment
     DBuf<uint32_t> xset, xbit;
     uint64_t n_extra = 0;
+    // member signatures (huffman_dev.cuh sig_mask): count x u64; all ones for sets appended
+    // from host bytes (members unknown), 0 for hybrid bitmap sets (they have their own pass)
+    DBuf<uint64_t> sig;
+    uint32_t sig_k = default_sig_k();  // bits per member (IMMX_SIG_K = 1..3; 0: no signatures, every live set is decoded)
     uint64_t device_bytes() const {  // the store as held in HBM, side index included
-        return total_words * 4 + total_copied * 4 + (count + 1) * 16 + count * (4 + 4 + 4 + 1 + 4) + n_extra * 8 +
+        return total_words * 4 + total_copied * 4 + (count + 1) * 16 + count * (4 + 4 + 4 + 1 + 4 + (sig_k ? 8 : 0)) + n_extra * 8 +
                dense_count * 4;
     }
     DBuf<uint64_t> coff;   // count+1

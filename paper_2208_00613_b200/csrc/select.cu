@@ -28,7 +28,10 @@ unsigned grid_for(uint64_t items, const Device& d) {
 // ---- select_huffman rounds (select.cpp:150-230) ------------------------------------
 // The reference decodes every live set per round: hits are deleted, misses recounted into a
 // fresh table.  The device splits a round in two passes with the same result:
-//   find  : decode each live set up to `pick` (no table writes); hits are deleted (marked
+//   filter: the live sets whose member signature (huffman_dev.cuh sig_mask, written by the
+//           encoder) holds the pick's bits become the round's decode candidates -- every set
+//           that holds the pick passes, the others only as false positives;
+//   find  : decode each candidate up to `pick` (no table writes); hits are deleted (marked
 //           with the round) and listed, and the member volume of the hits (H) is summed;
 //   apply : the table over the live sets is either the old one minus the hits' members
 //           (cost H) or a recount of the misses (cost M = live volume - H) into the other,
@@ -52,8 +55,10 @@ struct RoundCtl {           // device control block of one select_huffman call
     unsigned long long live_vol;  // member volume of the live sets (before this round)
     unsigned long long live_snap; // live_vol as the round's find pass saw it
     unsigned long long queue[2];  // work queues of the find and apply passes
-    unsigned long long nlist[2];  // item lists: the items the round's find pass took
+    unsigned long long ncand;     // decode candidates of the round (items: the filter's output)
     unsigned long long nhitx;     // extra segments of this round's hits
+    unsigned long long hbytes;    // payload bytes of this round's hits
+    unsigned long long live_bytes;  // payload bytes of the live sets (before this round)
 };
 
 __device__ __forceinline__ void warp_add_u64(unsigned long long* p, unsigned long long x) {
@@ -117,8 +122,7 @@ template <class Src, class Op>
 __device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict__ queue, const Src& srcs,
                                                   uint64_t total, const SegView& sv,
                                                   const unsigned long long* __restrict__ lut, uint32_t root_bits,
-                                                  Op& op, uint32_t* __restrict__ out_list = nullptr,
-                                                  unsigned long long* __restrict__ out_cnt = nullptr) {
+                                                  Op& op) {
     // chunks of up to 64 items, fewer when the pass is small (every warp should get work)
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t kChunk = (uint32_t)max((uint64_t)1, min((uint64_t)64, total / (nwarps * 2)));
@@ -154,7 +158,7 @@ __device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict
                 const bool lv = i < hi && op.live(jc);
                 uint32_t cbits = 0, cbit0 = 0, cbase = 0, clim = 0xffffffffu;
                 uint64_t cwo = 0;
-                if (i < hi) {
+                if (lv) {
                     cbits = sv.bits[jc];
                     cwo = sv.woff[jc];
                     if (it < sv.count) {
@@ -187,13 +191,6 @@ __device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict
                     base = basesrc;
                     lim = limsrc;
                     wo = wosrc;
-                }
-                if (out_list) {  // the taken items are the next round's candidates
-                    const uint32_t A = __ballot_sync(FULL, assign);
-                    unsigned long long ob = 0;
-                    if (lane == 0 && A) ob = atomicAdd(out_cnt, (unsigned long long)__popc(A));
-                    ob = __shfl_sync(FULL, ob, 0);
-                    if (assign) out_list[ob + __popc(A & lt)] = isrc;
                 }
                 cur += take < (uint32_t)__popc(L) ? nth_set_bit(L, take) : 32;
                 idle = __ballot_sync(FULL, !active);
@@ -234,6 +231,7 @@ __device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict
 
 struct FindOp {
     const uint32_t* deleted;
+    const uint32_t* bits;
     const uint64_t* coff;
     const uint32_t* copied;
     const uint32_t* msize;
@@ -247,7 +245,7 @@ struct FindOp {
     RoundCtl* ctl;
     uint32_t pick, mark;
     uint64_t maxd = 0;
-    unsigned long long hv = 0, by = 0;
+    unsigned long long hv = 0, hb = 0;
     __device__ bool live(uint32_t j) const { return deleted[j] == 0; }
     __device__ bool sym(bool have, uint32_t v, uint32_t) const { return have && v == pick; }
     __device__ void hit(uint32_t j, uint32_t decoded) {
@@ -260,6 +258,7 @@ struct FindOp {
         }
         hitnd[j] = decoded;
         hv += msize[j];
+        hb += (bits[j] + 7) / 8 + 4 * (coff[j + 1] - coff[j]);
         maxd = decoded > maxd ? decoded : maxd;
     }
     __device__ void end(uint32_t j, bool seg0, bool stopped, uint32_t idx, uint32_t nbits) {
@@ -270,7 +269,6 @@ struct FindOp {
         if (!seg0) return;
         // once per set: the uncodable members, searched after the whole stream
         const uint64_t c0 = coff[j], c1 = coff[j + 1];
-        by += (nbits + 7) / 8 + 4 * (c1 - c0);
         for (uint64_t c = c0; c < c1; ++c)
             if (copied[c] == pick) {
                 hit(j, ncw[j]);
@@ -279,7 +277,46 @@ struct FindOp {
     }
 };
 
-__global__ void k_huff_find(SegView sv, uint64_t total, uint32_t* __restrict__ list0, uint32_t* __restrict__ list1,
+// filter pass: one thread per set; a live set whose signature holds the pick's bits is listed
+// as a decode candidate, segment 0 followed by its extra segments
+__global__ void k_sig_filter(const uint64_t* __restrict__ sig, uint32_t sig_k, const uint32_t* __restrict__ deleted,
+                             const uint8_t* __restrict__ segd, const uint32_t* __restrict__ xfirst,
+                             const uint32_t* __restrict__ ncw, uint64_t count, RoundCtl* ctl,
+                             uint32_t* __restrict__ cand) {
+    const uint32_t pick = ctl->pick;
+    if (pick == 0xffffffffu) return;
+    const uint64_t m = sig_mask(pick, sig_k);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t j0 = w * 32; j0 < count; j0 += nw * 32) {
+        const uint64_t j = j0 + lane;
+        const bool c = j < count && deleted[j] == 0 && (sig[j] & m) == m;
+        if (!__any_sync(FULL, c)) continue;
+        uint32_t nx = 0, x0 = 0;
+        if (c && segd[j]) {
+            nx = (ncw[j] - 1) / kSegCodewords;
+            x0 = xfirst[j];
+        }
+        const uint32_t need = c ? 1u + nx : 0u;
+        uint32_t x = need;  // inclusive scan over the warp
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        const uint32_t tot = __shfl_sync(FULL, x, 31);
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(&ctl->ncand, (unsigned long long)tot);
+        b = __shfl_sync(FULL, b, 0) + x - need;
+        if (c) {
+            cand[b] = (uint32_t)j;
+            for (uint32_t t = 0; t < nx; ++t) cand[b + 1 + t] = (uint32_t)(count + x0 + t);
+        }
+    }
+}
+
+__global__ void k_huff_find(SegView sv, uint64_t total, const uint32_t* __restrict__ cand,
                             const uint64_t* __restrict__ coff, const uint32_t* __restrict__ copied,
                             const uint32_t* __restrict__ msize, const uint32_t* __restrict__ ncw,
                             const uint8_t* __restrict__ segd, const uint32_t* __restrict__ xfirst,
@@ -301,16 +338,14 @@ __global__ void k_huff_find(SegView sv, uint64_t total, uint32_t* __restrict__ l
             ctl->live_snap = ctl->live_vol;
         }
     }
-    FindOp op{deleted, coff, copied, msize, ncw, deleted, hitlist, hitnd, hitx, segd, xfirst, ctl, pick, r + 1};
-    // round 0 walks every item and lists the ones it took (live at that point: the sets the
-    // first pick covers -- on hub-dominated inputs most of the large ones -- drop out);
-    // later rounds walk that list
-    if (r == 0)
-        warp_decode_items(&ctl->queue[0], RangeSrc{}, total, sv, lut, root_bits, op, list0, &ctl->nlist[0]);
+    FindOp op{deleted, sv.bits, coff, copied, msize, ncw, deleted, hitlist, hitnd, hitx, segd, xfirst, ctl, pick, r + 1};
+    // the filter's candidates; without signatures (IMMX_SIG_K=0) every item
+    if (cand)
+        warp_decode_items(&ctl->queue[0], ListSrc{cand}, ctl->ncand, sv, lut, root_bits, op);
     else
-        warp_decode_items(&ctl->queue[0], ListSrc{list0}, ctl->nlist[0], sv, lut, root_bits, op);
+        warp_decode_items(&ctl->queue[0], RangeSrc{}, total, sv, lut, root_bits, op);
     warp_add_u64(&ctl->hvol, op.hv);
-    warp_add_u64(alg_bytes, op.by);
+    warp_add_u64(&ctl->hbytes, op.hb);
     uint64_t local_max = op.maxd;
     for (int o = 16; o; o >>= 1) local_max = max(local_max, (uint64_t)__shfl_xor_sync(FULL, local_max, o));
     if ((threadIdx.x & 31) == 0 && local_max) atomicMax(maxdec, (unsigned long long)local_max);
@@ -371,8 +406,7 @@ struct ApplyOp {
 // apply pass: the smaller of "subtract the hits" (H) and "recount the misses into the cleared
 // spare table" (M); block 0 publishes the choice and the table that is now live.  Also the
 // round's decode-buffer ledger entry for the misses (every codeword of a miss is decoded).
-__global__ void k_huff_apply(SegView sv, const uint32_t* __restrict__ list0, const uint32_t* __restrict__ list1,
-                             const uint32_t* __restrict__ hitlist, const uint32_t* __restrict__ hitx,
+__global__ void k_huff_apply(SegView sv, uint64_t total, const uint32_t* __restrict__ hitlist, const uint32_t* __restrict__ hitx,
                              const uint64_t* __restrict__ coff,
                              const uint32_t* __restrict__ copied, const uint32_t* __restrict__ ncw,
                              const unsigned long long* __restrict__ lut, uint32_t root_bits, RoundCtl* ctl,
@@ -390,6 +424,11 @@ __global__ void k_huff_apply(SegView sv, const uint32_t* __restrict__ list0, con
         ctl->apply = recount ? kApplyRecount : kApplySub;
         ctl->cur = recount ? cur ^ 1u : cur;
         ctl->live_vol = M;
+        // algorithmic bytes of the find: the reference decodes every live set;
+        // the hits stop at the pick and are not counted, as before the signature filter
+        const unsigned long long lb = ctl->live_bytes - ctl->hbytes;
+        atomicAdd(alg_bytes, lb);
+        ctl->live_bytes = lb;
     }
     unsigned int* live = cur ? hist1 : hist0;
     unsigned int* spare = cur ? hist0 : hist1;
@@ -404,9 +443,8 @@ __global__ void k_huff_apply(SegView sv, const uint32_t* __restrict__ list0, con
     }
     const uint32_t pick = ctl->pick;
     if (recount) {
-        // the live sets' items are among the items this round's find pass took
         ApplyOp op{deleted, coff, copied, spare, 1u, 0u, 0xffffffffu};
-        warp_decode_items(&ctl->queue[1], ListSrc{list0}, ctl->nlist[0], sv, lut, root_bits, op);
+        warp_decode_items(&ctl->queue[1], RangeSrc{}, total, sv, lut, root_bits, op);
         warp_add_u64(alg_bytes, op.by);
     } else {
         ApplyOp op{deleted, coff, copied, live, 0xffffffffu, r + 1, pick};
@@ -664,6 +702,8 @@ __global__ void k_argmax_pick(const unsigned int* __restrict__ hist0, const unsi
     }
     ctl->nhit = 0;
     ctl->nhitx = 0;
+    ctl->ncand = 0;
+    ctl->hbytes = 0;
     ctl->hvol = 0;
     ctl->queue[0] = ctl->queue[1] = 0;
     ctl->done = 0;
@@ -713,19 +753,21 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
     CK(cudaMemsetAsync(keys.p, 0, k * 8, s));
     CK(cudaMemsetAsync(mdec.p, 0, k * 8, s));
     const uint64_t items = theta + S.n_extra;
-    DBuf<uint32_t> seeds, hitlist, hitnd, hitx, list0, list1;  // list1: unused (kept for the signature)
+    DBuf<uint32_t> seeds, hitlist, hitnd, hitx, cand;
     seeds.exact(k);
     hitlist.exact(theta);
     hitnd.exact(theta);
     hitx.exact(std::max<uint64_t>(S.n_extra, 1));
-    list0.exact(items);
-    list1.exact(1);
+    const bool filter = S.sig_k != 0;
+    if (filter) cand.exact(items);
     DBuf<unsigned long long> ctlbuf;
     ctlbuf.exact((sizeof(RoundCtl) + 7) / 8);
     RoundCtl* ctl = reinterpret_cast<RoundCtl*>(ctlbuf.p);
     {
         RoundCtl h{};
         h.live_vol = 0;
+        // payload of the Huffman-coded sets (the bitmap sets are counted by the k_dense_* passes)
+        h.live_bytes = S.payload_bytes - S.dense_count * 4 * ((n + 31) / 32);
         CK(cudaMemcpyAsync(ctl, &h, sizeof(h), cudaMemcpyHostToDevice, s));
     }
     // live member volume = sum of msize
@@ -750,13 +792,16 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
     for (uint32_t r = 0; r < k; ++r) {
         k_argmax_pick<<<grid_am, 256, 0, s>>>(d_hist, hist_b.p, n, ctl, keys.p, r, is_seed.p, seeds.p, marg.p);
         kt[r].start(&d, IMMX_KSTAT_HSELECT);
-        k_huff_find<<<grid, 256, 0, s>>>(sv, items, list0.p, list1.p, S.coff.p, S.copied.p, S.msize.p, S.ncw.p,
+        if (filter)
+            k_sig_filter<<<grid_for(theta, d), 256, 0, s>>>(S.sig.p, S.sig_k, deleted.p, S.segd.p, S.xfirst.p, S.ncw.p,
+                                                           theta, ctl, cand.p);
+        k_huff_find<<<grid, 256, 0, s>>>(sv, items, filter ? cand.p : nullptr, S.coff.p, S.copied.p, S.msize.p, S.ncw.p,
                                          S.segd.p, S.xfirst.p, S.lut.p, S.lut_root_bits, ctl, deleted.p, r,
                                          hitlist.p, hitx.p, hitnd.p, mdec.p + r, rbytes.p + r, d_hist, hist_b.p, n);
         if (nd)
             k_dense_find<<<grid_for(nd, d), 256, 0, s>>>(S.words.p, S.woff.p, S.dense_ids.p, S.msize.p, nd, ctl,
                                                          deleted.p, r, hitnd.p, rbytes.p + r);
-        k_huff_apply<<<grid, 256, 0, s>>>(sv, list0.p, list1.p, hitlist.p, hitx.p, S.coff.p, S.copied.p, S.ncw.p,
+        k_huff_apply<<<grid, 256, 0, s>>>(sv, items, hitlist.p, hitx.p, S.coff.p, S.copied.p, S.ncw.p,
                                           S.lut.p, S.lut_root_bits, ctl, deleted.p, r, d_hist, hist_b.p, n,
                                           mdec.p + r, rbytes.p + r);
         if (nd)
@@ -767,12 +812,12 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
             RoundCtl h;
             CK(cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
-            std::fprintf(stderr, "[immx select] round %u pick %u apply %u hits %llu H %llu live %llu\n", r, h.pick,
-                         h.apply, (unsigned long long)h.nhit, (unsigned long long)h.hvol,
-                         (unsigned long long)h.live_vol);
+            std::fprintf(stderr, "[immx select] round %u pick %u apply %u cand %llu hits %llu H %llu live %llu\n", r,
+                         h.pick, h.apply, (unsigned long long)h.ncand, (unsigned long long)h.nhit,
+                         (unsigned long long)h.hvol, (unsigned long long)h.live_vol);
         }
         CK_LAUNCH("select_huffman round");
-        d.kernel_launches += 3 + (nd ? 2 : 0);
+        d.kernel_launches += 3 + (filter ? 1 : 0) + (nd ? 2 : 0);
     }
     tq("rounds");
     std::vector<unsigned long long> hbytes(k);
