@@ -202,8 +202,10 @@ typedef struct {
     double covered_fraction;
     uint64_t estimation_samples;
 } immx_plan;
-/* sampler.cpp:106-161 estimate_theta.  If keep != NULL the estimation pool (global
- * indices [0, estimation_samples)) is left in it for reuse. */
+/* sampler.cpp:106-161 estimate_theta.  If keep != NULL the estimation pool is left in it for
+ * reuse: global indices [0, count) with count >= estimation_samples (immx_pool_info) -- the
+ * loop may have drawn the sets of later iterations in one launch (look-ahead sampling); set j
+ * is the reference's set j either way. */
 IMMX_API int immx_estimate_theta(const immx_graph* g, uint32_t k, double epsilon, uint64_t seed, int model,
                         immx_pool* keep, immx_plan* out);
 

@@ -119,19 +119,49 @@ void estimate_theta_dev(const DevGraph& G, uint32_t k, double eps, uint64_t seed
     plan.k = k;
     plan.epsilon = eps;
     plan.rng_seed = seed;
+    // Look-ahead sampling.  Iteration i's exit test needs the sets [0, theta_i) whatever the
+    // earlier tests said, so the only way to draw a set the reference would not is to run past
+    // the iteration that exits.  The covered fraction barely moves between iterations while the
+    // threshold halves: an iteration whose threshold is above `margin` x the last measured
+    // fraction is taken not to exit, and the sets of the iterations after it are drawn in the
+    // same launch (fewer launches: each ends on a tail of giant samples, ~85 ms on config 5).
+    // Every test still runs, in order, on exactly its first theta_i sets.  A wrong guess only
+    // leaves extra sets in the pool (a set is a pure function of (seed, index)); the plan and
+    // every result are the reference's.  IMMX_LOOKAHEAD: margin (default 1.25), 0 = off,
+    // "force" = always draw two iterations ahead (tests: a pool holding more than theta).
+    const double la_margin = [] {  // (read per call: the tests switch it)
+        const char* e = std::getenv("IMMX_LOOKAHEAD");
+        if (!e || !*e) return 1.25;
+        if (!std::strcmp(e, "force")) return -1.0;
+        const double v = std::strtod(e, nullptr);
+        return v >= 1.0 ? v : 0.0;
+    }();
+    auto theta_of = [&](uint32_t i) { return (uint64_t)std::ceil(base * std::exp2((double)i)); };
     uint64_t sampled = pool.count;  // a caller may hand over a pool already holding [0, count)
-    double lower_bound = 0.0;
+    const uint64_t sampled_at_entry = sampled;
+    double lower_bound = 0.0, last_fraction = -1.0;
+    uint64_t theta_exit = 0;
     for (uint32_t i = 1; i <= i_max; ++i) {
-        const uint64_t theta_i = (uint64_t)std::ceil(base * std::exp2((double)i));
+        const uint64_t theta_i = theta_of(i);
+        theta_exit = std::max(theta_exit, theta_i);
         if (theta_i > sampled) {
-            sample_into_pool(pool, G, theta_i - sampled, sampled, seed, nullptr, nullptr, model);
-            sampled = theta_i;
+            uint32_t j = i;
+            if (la_margin < 0.0) {
+                j = std::min(i + 2, i_max);
+            } else if (la_margin > 0.0 && last_fraction >= 0.0) {
+                while (j < i_max && last_fraction * la_margin < (1.0 + eps_prime) / std::exp2((double)j)) ++j;
+            }
+            const uint64_t upto = theta_of(j);
+            sample_into_pool(pool, G, upto - sampled, sampled, seed, nullptr, nullptr, model);
+            sampled = upto;
         }
         SelectOut sel;
-        // select over exactly the first theta_i-or-more sets (the pool holds [0, sampled))
-        select_raw_dev(pool, n, k, sel);
+        // select over exactly the first theta_i sets (a pool handed over by the caller with more
+        // than theta_i sets is used whole, as before)
+        select_raw_dev(pool, n, k, sel, std::max(theta_i, sampled_at_entry));
         const double covered = sel.coverage.empty() ? 0.0 : sel.coverage.back();
         plan.covered_fraction = covered;
+        last_fraction = covered;
         const double x_i = (double)n / std::exp2((double)i);
         if ((double)n * covered >= (1.0 + eps_prime) * x_i) {
             plan.exit_iteration = i;
@@ -139,6 +169,8 @@ void estimate_theta_dev(const DevGraph& G, uint32_t k, double eps, uint64_t seed
             break;
         }
     }
+    // sampler.cpp:156: the sets the reference has drawn when the loop ends
+    sampled = std::max(theta_exit, sampled_at_entry);
     plan.estimation_samples = sampled;
     if (plan.exit_iteration != 0) {
         const uint64_t bound = (uint64_t)std::ceil(base * (double)n / lower_bound);
@@ -1034,11 +1066,15 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                                      (unsigned long long)leaves.size(), t_leaves, t_codebook - t_leaves);
                     // the decode table is needed only by the selection: build it on a host
                     // thread while the device encodes the blocks
-                    lut_job = std::async(std::launch::async, [&cb, &d, &lut_rb, &t_lut, secs]() {
-                        const auto tl = Clock::now();
-                        build_decode_lut(cb, d.run_lut, lut_rb);
-                        t_lut = secs(tl);
-                    });
+                    // IMMX_LUT_HOST=1: the host builder (codebook.cpp), on a thread beside the encode
+                    const char* lh = std::getenv("IMMX_LUT_HOST");
+                    const bool device_lut = !(lh && *lh && *lh != '0');
+                    if (!device_lut)
+                        lut_job = std::async(std::launch::async, [&cb, &d, &lut_rb, &t_lut, secs]() {
+                            const auto tl = Clock::now();
+                            build_decode_lut(cb, d.run_lut, lut_rb);
+                            t_lut = secs(tl);
+                        });
                     if (!d.run_store) d.run_store = new immx_store;
                     store = d.run_store;
                     store->s.count = store->s.total_words = store->s.total_copied = store->s.payload_bytes = 0;
@@ -1046,7 +1082,11 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
                     store->s.n_extra = 0;
                     store->s.sig_k = default_sig_k();
                     store->s.hybrid = mode == IMMX_MODE_HYBRID;
-                    store_set_leaf_codes(store->s, d, n, cb, {}, 1);
+                    {
+                        const auto tl = Clock::now();
+                        store_set_leaf_codes(store->s, d, n, cb, {}, 1, device_lut);
+                        if (device_lut) t_lut = secs(tl);  // (codes upload + scatter + table)
+                    }
                 } else if (mode == IMMX_MODE_BITMAP) {
                     bm.reset(new immx_bitmap);
                     bm->b.dev = &d;
@@ -1075,7 +1115,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
             ckpt();
             if (mode != IMMX_MODE_RAW) {
                 led_raw -= raw;
-                if (hi >= pool.count) {  // every pooled set is encoded: release the raw sets
+                if (hi >= pool.count || done == theta) {  // every set of the run in the pool is encoded: release the raw sets
                     edges_released += pool.edges;
                     pool_release(pool);
                     pool_base = ghi;
@@ -1104,6 +1144,9 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
             if (std::getenv("IMMX_DEBUG_CODEBOOK"))
                 std::fprintf(stderr, "[immx codebook] decode table %zu entries (root %u bits) %.4f s, nodes %zu\n",
                              d.run_lut.size(), lut_rb, t_lut, cb.nodes.size());
+        } else if (store && std::getenv("IMMX_DEBUG_CODEBOOK")) {
+            std::fprintf(stderr, "[immx codebook] decode table (device) %llu entries (root %u bits), codes + table %.4f s\n",
+                         (unsigned long long)store->s.lut_entries, store->s.lut_root_bits, t_lut);
         }
 
         // ---- selection (pipeline.cpp:156-175) ----
@@ -1112,7 +1155,7 @@ int immx_run(const immx_graph* gh, const immx_run_config* cfg, immx_result** out
         ckpt();
         SelectOut sel;
         if (mode == IMMX_MODE_RAW) {
-            select_raw_dev(pool, n, k, sel);
+            select_raw_dev(pool, n, k, sel, theta);  // (the pool may hold look-ahead sets past theta)
         } else if (mode == IMMX_MODE_HUFFMAN || mode == IMMX_MODE_HYBRID) {
             std::vector<uint64_t> md;
             select_huffman_dev(store->s, hist.p, k, sel, &md);

@@ -7,6 +7,7 @@
 // the host (it is ~2% of the reference's time, and strictly sequential); the
 // device receives the per-vertex codes and a multi-level lookup table.
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.hpp"
 
@@ -137,7 +138,9 @@ HostCodebook build_codebook_host(const uint64_t* freq, uint64_t n) {
 }
 
 // Multi-level decode table (entry layout: huffman.cu header).  Table widths: root
-// min(12, height), sub-tables min(8, height of the subtree below the boundary node).
+// min(16, height), sub-tables min(12, height of the subtree below the boundary node) -- two
+// dependent lookups for codes up to 28 bits (12 / 8 until round 2: three for c4's 17-26-bit
+// codes; c4 select -8%, table 5.07 M -> 5.59 M entries).  IMMX_LUT_ROOT / IMMX_LUT_SUB override.
 void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& lut, uint32_t& root_bits) {
     const size_t nn = cb.nodes.size();
     // subtree heights: children before parents in one index sweep
@@ -155,7 +158,13 @@ void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& l
     else
         for (size_t u = nn; u-- > 0;) upd(u);
     lut.clear();  // keeps its capacity
-    root_bits = std::max<uint32_t>(1, std::min<uint32_t>(12, height[cb.root]));
+    auto width_knob = [](const char* name, uint32_t dflt) {
+        const char* e = std::getenv(name);
+        const long v = e && *e ? std::strtol(e, nullptr, 10) : 0;
+        return v >= 1 && v <= 20 ? (uint32_t)v : dflt;
+    };
+    const uint32_t root_max = width_knob("IMMX_LUT_ROOT", 16), sub_max = width_knob("IMMX_LUT_SUB", 12);
+    root_bits = std::max<uint32_t>(1, std::min<uint32_t>(root_max, height[cb.root]));
     struct Job {
         int32_t node;
         uint32_t width;
@@ -187,7 +196,7 @@ void build_decode_lut(const HostCodebook& cb, std::vector<unsigned long long>& l
                 const uint64_t span = 1ULL << (jb.width - f.depth);
                 std::fill(lut.begin() + jb.offset + f.prefix * span, lut.begin() + jb.offset + (f.prefix + 1) * span, e);
             } else if (f.depth == jb.width) {
-                const uint32_t w = std::max<uint32_t>(1, std::min<uint32_t>(8, height[f.node]));
+                const uint32_t w = std::max<uint32_t>(1, std::min<uint32_t>(sub_max, height[f.node]));
                 const uint64_t off = lut.size();
                 lut.resize(off + (1ULL << w), 0ULL);
                 jobs.push_back({f.node, w, off});

@@ -10,7 +10,7 @@
 // ceil(bits/8) + 4*|copied| (huffman.hpp:44); the device bytes are reported separately.
 //
 // Decoding uses a multi-level lookup table derived from the (non-canonical) tree: the root
-// table indexes the next 12 bits, sub-tables up to 8 bits.  Entry layout (u64):
+// table indexes the next 16 bits, sub-tables up to 12 bits (codebook.cpp).  Entry layout (u64):
 //   leaf    : bit63=1, bits56..62 = bits consumed at this level, bits0..31 = symbol
 //   pointer : bit63=0, bit62=1, bits56..61 = sub-table width, bits0..47 = sub-table offset
 //   invalid : 0 (a prefix that is no codeword)
@@ -259,7 +259,7 @@ __global__ void k_add2(uint64_t* __restrict__ a, uint64_t* __restrict__ b, uint6
 }  // namespace
 
 void store_set_leaf_codes(Store& S, Device& d, uint64_t n, const HostCodebook& cb,
-                          const std::vector<unsigned long long>& lut, uint32_t root_bits) {
+                          const std::vector<unsigned long long>& lut, uint32_t root_bits, bool device_lut) {
     cudaStream_t s = d.stream;
     S.dev = &d;
     S.n = n;
@@ -280,12 +280,17 @@ void store_set_leaf_codes(Store& S, Device& d, uint64_t n, const HostCodebook& c
         k_scatter_codes<<<grid_for(L, d), 256, 0, s>>>(sym.p, bits.p, len.p, L, S.code_bits.p, S.code_len.p);
         CK_LAUNCH("k_scatter_codes");
         d.kernel_launches++;
+        if (device_lut) store_build_lut_dev(S, d, sym.p, bits.p, len.p, L);
         CK(cudaStreamSynchronize(s));  // the leaf buffers go out of scope
+    } else if (device_lut) {
+        store_build_lut_dev(S, d, nullptr, nullptr, nullptr, 0);
     }
-    S.lut.exact(std::max<uint64_t>(lut.size(), 1));
-    if (!lut.empty()) CK(cudaMemcpyAsync(S.lut.p, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice, s));
-    S.lut_root_bits = root_bits;
-    S.lut_entries = lut.size();
+    if (!device_lut) {
+        S.lut.exact(std::max<uint64_t>(lut.size(), 1));
+        if (!lut.empty()) CK(cudaMemcpyAsync(S.lut.p, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice, s));
+        S.lut_root_bits = root_bits;
+        S.lut_entries = lut.size();
+    }
     S.woff.reserve(1, s);
     S.coff.reserve(1, s);
     uint64_t z = 0;

@@ -285,7 +285,10 @@ struct Store {
     DBuf<uint32_t> dense_ids;  // store indices of the dense sets
 };
 constexpr uint32_t kDenseBits = 0xffffffffu;
-constexpr uint32_t kSegCodewords = 64;
+#ifndef IMMX_SEG_CW
+#define IMMX_SEG_CW 64
+#endif
+constexpr uint32_t kSegCodewords = IMMX_SEG_CW;
 
 
 // ---------------------------------------------------------------- device operations ----
@@ -316,14 +319,18 @@ void u32_to_u64_dev(Device& d, const unsigned int* a, uint64_t n, uint64_t* b);
 void u64_to_u32_dev(Device& d, const uint64_t* a, uint64_t n, unsigned int* b);
 void finish_select(const std::vector<uint32_t>& seeds, const std::vector<unsigned long long>& marg, uint64_t theta,
                    SelectOut& out);
-void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out);
+void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out, uint64_t upto = ~0ull);
 void pool_read_host(const Pool& P, uint64_t lo, uint64_t hi, uint64_t* offsets, uint32_t* members);
 void pool_upload_host(Pool& P, const uint64_t* offsets, const uint32_t* members, uint64_t count, uint64_t n_check);
 // huffman.cu
 struct HostCodebook;
 // the codes of the coded vertices only (scattered on the device; every other vertex uncoded)
+// (device_lut: the decode table is built on the device from the codes, lut_dev.cu)
 void store_set_leaf_codes(Store& S, Device& d, uint64_t n, const HostCodebook& cb,
-                          const std::vector<unsigned long long>& lut, uint32_t root_bits);
+                          const std::vector<unsigned long long>& lut, uint32_t root_bits, bool device_lut = false);
+// lut_dev.cu: the decode table from the codes of the L coded vertices (device arrays, any order)
+void store_build_lut_dev(Store& S, Device& d, const uint32_t* d_sym, const uint64_t* d_bits, const uint8_t* d_len,
+                         uint64_t L);
 void store_set_lut(Store& S, Device& d, const std::vector<unsigned long long>& lut, uint32_t root_bits);
 // vertices counted in the table (hist > 0) that have no code
 uint64_t count_uncoded_dev(Device& d, const unsigned int* d_hist, const uint8_t* d_code_len, uint64_t n);

@@ -61,6 +61,15 @@ struct RoundCtl {           // device control block of one select_huffman call
     unsigned long long live_bytes;  // payload bytes of the live sets (before this round)
 };
 
+// grid-wide clear of a table of n counters (16-byte stores; the tables are allocation-aligned)
+__device__ __forceinline__ void grid_clear_u32(unsigned int* __restrict__ t, uint64_t n) {
+    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gs = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t n4 = n / 4;
+    uint4* t4 = reinterpret_cast<uint4*>(t);
+    for (uint64_t q = gt; q < n4; q += gs) t4[q] = make_uint4(0u, 0u, 0u, 0u);
+    for (uint64_t v = n4 * 4 + gt; v < n; v += gs) t[v] = 0;
+}
+
 __device__ __forceinline__ void warp_add_u64(unsigned long long* p, unsigned long long x) {
     for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
     if ((threadIdx.x & 31) == 0 && x) atomicAdd(p, x);
@@ -125,6 +134,8 @@ __device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict
                                                   Op& op) {
     // chunks of up to 64 items, fewer when the pass is small (every warp should get work)
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    // (small passes spread one item per warp: a warp with few active lanes steps faster than a
+    // full one -- chunks of at least 32 measured c3 find +15%, apply +43%)
     const uint32_t kChunk = (uint32_t)max((uint64_t)1, min((uint64_t)64, total / (nwarps * 2)));
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
@@ -158,7 +169,7 @@ __device__ __forceinline__ void warp_decode_items(unsigned long long* __restrict
                 const bool lv = i < hi && op.live(jc);
                 uint32_t cbits = 0, cbit0 = 0, cbase = 0, clim = 0xffffffffu;
                 uint64_t cwo = 0;
-                if (lv) {
+                if (i < hi) {
                     cbits = sv.bits[jc];
                     cwo = sv.woff[jc];
                     if (it < sv.count) {
@@ -277,42 +288,67 @@ struct FindOp {
     }
 };
 
-// filter pass: one thread per set; a live set whose signature holds the pick's bits is listed
-// as a decode candidate, segment 0 followed by its extra segments
-__global__ void k_sig_filter(const uint64_t* __restrict__ sig, uint32_t sig_k, const uint32_t* __restrict__ deleted,
-                             const uint8_t* __restrict__ segd, const uint32_t* __restrict__ xfirst,
-                             const uint32_t* __restrict__ ncw, uint64_t count, RoundCtl* ctl,
-                             uint32_t* __restrict__ cand) {
+// filter pass: a thread tests four consecutive sets (vector loads of the live flags and the
+// signatures); a live set whose signature holds the pick's bits is listed as a decode
+// candidate, segment 0 followed by its extra segments.  One list-cursor atomic per CTA tile.
+constexpr uint32_t kFilterThreads = 256;
+__global__ void __launch_bounds__(kFilterThreads)
+k_sig_filter(const uint64_t* __restrict__ sig, uint32_t sig_k, const uint32_t* __restrict__ deleted,
+             const uint8_t* __restrict__ segd, const uint32_t* __restrict__ xfirst, const uint32_t* __restrict__ ncw,
+             uint64_t count, RoundCtl* ctl, uint32_t* __restrict__ cand) {
     const uint32_t pick = ctl->pick;
     if (pick == 0xffffffffu) return;
     const uint64_t m = sig_mask(pick, sig_k);
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t j0 = w * 32; j0 < count; j0 += nw * 32) {
-        const uint64_t j = j0 + lane;
-        const bool c = j < count && deleted[j] == 0 && (sig[j] & m) == m;
-        if (!__any_sync(FULL, c)) continue;
-        uint32_t nx = 0, x0 = 0;
-        if (c && segd[j]) {
-            nx = (ncw[j] - 1) / kSegCodewords;
-            x0 = xfirst[j];
+    using Scan = cub::BlockScan<uint32_t, kFilterThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ unsigned long long s_base;
+    const uint64_t tile = (uint64_t)kFilterThreads * 4;
+    for (uint64_t t0 = blockIdx.x * tile; t0 < count; t0 += (uint64_t)gridDim.x * tile) {
+        const uint64_t j0 = t0 + (uint64_t)threadIdx.x * 4;
+        uint32_t dl[4] = {1u, 1u, 1u, 1u};
+        uint64_t sg[4] = {0, 0, 0, 0};
+        if (j0 + 4 <= count) {
+            const uint4 d4 = *reinterpret_cast<const uint4*>(deleted + j0);
+            const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(sig + j0);
+            const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(sig + j0 + 2);
+            dl[0] = d4.x, dl[1] = d4.y, dl[2] = d4.z, dl[3] = d4.w;
+            sg[0] = a.x, sg[1] = a.y, sg[2] = b.x, sg[3] = b.y;
+        } else {
+            for (uint32_t q = 0; q < 4; ++q)
+                if (j0 + q < count) {
+                    dl[q] = deleted[j0 + q];
+                    sg[q] = sig[j0 + q];
+                }
         }
-        const uint32_t need = c ? 1u + nx : 0u;
-        uint32_t x = need;  // inclusive scan over the warp
+        uint32_t nx[4], x0[4], need = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(FULL, x, o);
-            if (lane >= (uint32_t)o) x += y;
+        for (uint32_t q = 0; q < 4; ++q) {
+            const bool c = dl[q] == 0 && (sg[q] & m) == m;
+            nx[q] = 0xffffffffu;  // not a candidate
+            x0[q] = 0;
+            if (c) {
+                nx[q] = 0;
+                if (segd[j0 + q]) {
+                    nx[q] = (ncw[j0 + q] - 1) / kSegCodewords;
+                    x0[q] = xfirst[j0 + q];
+                }
+                need += 1u + nx[q];
+            }
         }
-        const uint32_t tot = __shfl_sync(FULL, x, 31);
-        unsigned long long b = 0;
-        if (lane == 0) b = atomicAdd(&ctl->ncand, (unsigned long long)tot);
-        b = __shfl_sync(FULL, b, 0) + x - need;
-        if (c) {
-            cand[b] = (uint32_t)j;
-            for (uint32_t t = 0; t < nx; ++t) cand[b + 1 + t] = (uint32_t)(count + x0 + t);
+        uint32_t pre, tot;
+        Scan(tmp).ExclusiveSum(need, pre, tot);
+        if (threadIdx.x == 0 && tot) s_base = atomicAdd(&ctl->ncand, (unsigned long long)tot);
+        __syncthreads();
+        if (need) {
+            unsigned long long b = s_base + pre;
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q)
+                if (nx[q] != 0xffffffffu) {
+                    cand[b++] = (uint32_t)(j0 + q);
+                    for (uint32_t t = 0; t < nx[q]; ++t) cand[b++] = (uint32_t)(count + x0[q] + t);
+                }
         }
+        __syncthreads();  // tmp and s_base are reused by the next tile
     }
 }
 
@@ -331,8 +367,7 @@ __global__ void k_huff_find(SegView sv, uint64_t total, const uint32_t* __restri
         // the spare table is the recount target of this round: clear it while decoding
         const uint32_t cur = ctl->cur;
         unsigned int* spare = cur ? hist0 : hist1;
-        for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
-            spare[v] = 0;
+        grid_clear_u32(spare, n);
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             ctl->cur_snap = cur;
             ctl->live_snap = ctl->live_vol;
@@ -435,7 +470,14 @@ __global__ void k_huff_apply(SegView sv, uint64_t total, const uint32_t* __restr
     {
         // the misses: every codeword decoded (huffman.cpp:150-157)
         uint64_t m = 0;
-        for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < sv.count;
+        const uint64_t c4 = sv.count / 4;  // four sets per thread and step (vector loads)
+        for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < c4; q += (uint64_t)gridDim.x * blockDim.x) {
+            const uint4 dl = reinterpret_cast<const uint4*>(deleted)[q];
+            const uint4 cw = reinterpret_cast<const uint4*>(ncw)[q];
+            const uint32_t a = max(dl.x ? 0u : cw.x, dl.y ? 0u : cw.y), b = max(dl.z ? 0u : cw.z, dl.w ? 0u : cw.w);
+            m = max(m, (uint64_t)max(a, b));
+        }
+        for (uint64_t j = c4 * 4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < sv.count;
              j += (uint64_t)gridDim.x * blockDim.x)
             if (deleted[j] == 0) m = max(m, (uint64_t)ncw[j]);
         for (int o = 16; o; o >>= 1) m = max(m, (uint64_t)__shfl_xor_sync(FULL, m, o));
@@ -525,7 +567,7 @@ __global__ void k_raw_mark(const RawChunkView* __restrict__ chunks, uint32_t nch
     {
         const uint32_t cur = ctl->cur;
         unsigned int* spare = cur ? hist0 : hist1;
-        for (uint64_t v = gt; v < n; v += gs) spare[v] = 0;
+        grid_clear_u32(spare, n);
         if (gt == 0) {
             ctl->cur_snap = cur;
             ctl->live_snap = ctl->live_vol;
@@ -558,7 +600,7 @@ __global__ void k_raw_scan_mark(const uint32_t* __restrict__ arena, const uint64
     {
         const uint32_t cur = ctl->cur;
         unsigned int* spare = cur ? hist0 : hist1;
-        for (uint64_t v = gt; v < n; v += gs) spare[v] = 0;
+        grid_clear_u32(spare, n);
         if (gt == 0) {
             ctl->cur_snap = cur;
             ctl->live_snap = ctl->live_vol;
@@ -660,9 +702,19 @@ __global__ void k_argmax_pick(const unsigned int* __restrict__ hist0, const unsi
                               unsigned long long* __restrict__ marg) {
     const unsigned int* hist = ctl->cur ? hist1 : hist0;
     unsigned long long best = 0;
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
-        const unsigned long long key = ((unsigned long long)hist[v] << 32) | (0xffffffffu - (uint32_t)v);
+    auto take = [&](unsigned int c, uint64_t v) {
+        const unsigned long long key = ((unsigned long long)c << 32) | (0xffffffffu - (uint32_t)v);
         best = key > best ? key : best;
+    };
+    {
+        const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, gs = (uint64_t)gridDim.x * blockDim.x;
+        const uint64_t n4 = n / 4;  // four counters per load (the tables are allocation-aligned)
+        const uint4* h4 = reinterpret_cast<const uint4*>(hist);
+        for (uint64_t q = gt; q < n4; q += gs) {
+            const uint4 c = h4[q];
+            take(c.x, q * 4), take(c.y, q * 4 + 1), take(c.z, q * 4 + 2), take(c.w, q * 4 + 3);
+        }
+        for (uint64_t v = n4 * 4 + gt; v < n; v += gs) take(hist[v], v);
     }
     for (int o = 16; o; o >>= 1) {
         const unsigned long long x = __shfl_xor_sync(FULL, best, o);
@@ -787,20 +839,34 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
     DBuf<unsigned int> hist_b;  // the second table (recount target, double-buffered)
     hist_b.exact(n);
     const unsigned grid_am = grid_for(n, d);
+    const unsigned grid_filter =
+        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)d.num_sms * 8, (theta + 1023) / 1024));
     tq("setup");
     std::vector<KTimer> kt(k);
+    std::vector<cudaEvent_t> pe;  // IMMX_DEBUG_PHASES: an event between the kernels of every round
+    auto mark = [&]() {
+        if (!dbg_phases) return;
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, s));
+        pe.push_back(e);
+    };
     for (uint32_t r = 0; r < k; ++r) {
+        mark();
         k_argmax_pick<<<grid_am, 256, 0, s>>>(d_hist, hist_b.p, n, ctl, keys.p, r, is_seed.p, seeds.p, marg.p);
         kt[r].start(&d, IMMX_KSTAT_HSELECT);
+        mark();
         if (filter)
-            k_sig_filter<<<grid_for(theta, d), 256, 0, s>>>(S.sig.p, S.sig_k, deleted.p, S.segd.p, S.xfirst.p, S.ncw.p,
+            k_sig_filter<<<grid_filter, kFilterThreads, 0, s>>>(S.sig.p, S.sig_k, deleted.p, S.segd.p, S.xfirst.p, S.ncw.p,
                                                            theta, ctl, cand.p);
+        mark();
         k_huff_find<<<grid, 256, 0, s>>>(sv, items, filter ? cand.p : nullptr, S.coff.p, S.copied.p, S.msize.p, S.ncw.p,
                                          S.segd.p, S.xfirst.p, S.lut.p, S.lut_root_bits, ctl, deleted.p, r,
                                          hitlist.p, hitx.p, hitnd.p, mdec.p + r, rbytes.p + r, d_hist, hist_b.p, n);
         if (nd)
             k_dense_find<<<grid_for(nd, d), 256, 0, s>>>(S.words.p, S.woff.p, S.dense_ids.p, S.msize.p, nd, ctl,
                                                          deleted.p, r, hitnd.p, rbytes.p + r);
+        mark();
         k_huff_apply<<<grid, 256, 0, s>>>(sv, items, hitlist.p, hitx.p, S.coff.p, S.copied.p, S.ncw.p,
                                           S.lut.p, S.lut_root_bits, ctl, deleted.p, r, d_hist, hist_b.p, n,
                                           mdec.p + r, rbytes.p + r);
@@ -808,6 +874,7 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
             k_dense_apply<<<(unsigned)std::min<uint64_t>(nd, (uint64_t)d.num_sms * 8), 256, 0, s>>>(
                 S.words.p, S.woff.p, S.dense_ids.p, nd, nwd, ctl, deleted.p, r, d_hist, hist_b.p, rbytes.p + r);
         kt[r].stop();
+        mark();
         if (debug_select()) {
             RoundCtl h;
             CK(cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -820,6 +887,19 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
         d.kernel_launches += 3 + (filter ? 1 : 0) + (nd ? 2 : 0);
     }
     tq("rounds");
+    if (dbg_phases) {
+        CK(cudaStreamSynchronize(s));
+        double cls[4] = {0, 0, 0, 0};  // argmax+pick, filter, find, apply
+        for (uint32_t r = 0; r < k; ++r)
+            for (int c = 0; c < 4; ++c) {
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, pe[r * 5 + c], pe[r * 5 + c + 1]));
+                cls[c] += ms;
+            }
+        for (cudaEvent_t e : pe) cudaEventDestroy(e);
+        std::fprintf(stderr, "[immx select] %u rounds: argmax_pick %.3f ms, filter %.3f ms, find %.3f ms, apply %.3f ms\n", k,
+                     cls[0], cls[1], cls[2], cls[3]);
+    }
     std::vector<unsigned long long> hbytes(k);
     CK(cudaMemcpyAsync(hbytes.data(), rbytes.p, k * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -835,10 +915,24 @@ void select_huffman_dev(Store& S, unsigned int* d_hist, uint32_t k, SelectOut& o
 }
 
 // select.cpp:89-148 on the device (the estimation loop's greedy and raw mode).
-void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
+// `upto` < P.count selects over the first `upto` sets only (the estimation loop's exit tests
+// on a pool that already holds later iterations' sets).
+void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out, uint64_t upto) {
     Device& d = *P.dev;
     cudaStream_t s = d.stream;
-    const uint64_t theta = P.count;
+    const uint64_t theta = std::min<uint64_t>(P.count, upto);
+    uint64_t members = P.members;  // of the first theta sets
+    if (theta < P.count && theta) {
+        unsigned long long* sum = d.scal.p + 49;
+        size_t tb = 0;
+        cub::DeviceReduce::Sum(nullptr, tb, P.len.p, sum, (int64_t)theta, s);
+        d.tmp.reserve(tb, s, false);
+        CK(cub::DeviceReduce::Sum(d.tmp.p, tb, P.len.p, sum, (int64_t)theta, s));
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, sum, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        members = h;
+    }
     if (theta == 0) fail(IMMX_EINVAL, "selection requires at least one set");
     if (k >= n) fail(IMMX_EINVAL, "selection requires k < n");
     if (theta >= 0xffffffffULL) fail(IMMX_EINVAL, "more than 2^32-1 sets");
@@ -897,7 +991,8 @@ void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
         CK(cudaStreamSynchronize(s));
     };
     DBuf<unsigned int>& hist = d.ws_hist;  // the working table (+ its double)
-    hist.exact(2 * n);
+    const uint64_t npad = (n + 3) & ~3ull;  // the second table starts 16-byte aligned (vector loads)
+    hist.exact(2 * npad);
     CK(cudaMemcpyAsync(hist.p, X.hist.p, n * 4, cudaMemcpyDeviceToDevice, s));
     DBuf<uint32_t> covered, hitlist, seeds;  // covered: 0 live, r+1 covered in round r
     DBuf<uint8_t> is_seed;
@@ -915,7 +1010,7 @@ void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
     RoundCtl* ctl = reinterpret_cast<RoundCtl*>(ctlbuf.p);
     {
         RoundCtl h{};
-        h.live_vol = P.members;
+        h.live_vol = members;
         CK(cudaMemcpyAsync(ctl, &h, sizeof(h), cudaMemcpyHostToDevice, s));
     }
     const unsigned grid_am = grid_for(n, d), grid_w = (unsigned)d.num_sms * 8;
@@ -928,21 +1023,21 @@ void select_raw_dev(const Pool& P, uint64_t n, uint32_t k, SelectOut& out) {
             unsigned long long live = 0;
             CK(cudaMemcpyAsync(&live, &ctl->live_vol, 8, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
-            const uint64_t unindexed = P.members - X.indexed_members;
+            const uint64_t unindexed = members - X.indexed_members;
             scan = (uint64_t)live * (k - 1) < 4 * unindexed;
             if (!scan) build_index();
         }
-        k_argmax_pick<<<grid_am, 256, 0, s>>>(hist.p, hist.p + n, n, ctl, keys.p, r, is_seed.p, seeds.p, marg.p);
+        k_argmax_pick<<<grid_am, 256, 0, s>>>(hist.p, hist.p + npad, n, ctl, keys.p, r, is_seed.p, seeds.p, marg.p);
         kt[r].start(&d, IMMX_KSTAT_RSELECT);
         if (scan)
             k_raw_scan_mark<<<grid_w, 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, theta, ctl, covered.p, r, hitlist.p,
-                                                   hist.p, hist.p + n, n);
+                                                   hist.p, hist.p + npad, n);
         else
             k_raw_mark<<<grid_w, 256, 0, s>>>(reinterpret_cast<const RawChunkView*>(X.meta.p),
                                               (uint32_t)X.chunks.size(), ctl, covered.p, P.len.p, r, hitlist.p, hist.p,
-                                              hist.p + n, n);
+                                              hist.p + npad, n);
         k_raw_apply<<<grid_w, 256, 0, s>>>(P.arena.p, P.off.p, P.len.p, theta, ctl, covered.p, hitlist.p, hist.p,
-                                           hist.p + n, n);
+                                           hist.p + npad, n);
         kt[r].stop();
         CK_LAUNCH("select_raw round");
         d.kernel_launches += 3;
