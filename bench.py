@@ -461,7 +461,7 @@ def run_ours(args, cfg, rank, world, local):
                 e.record(stream)
                 marks.append(e)
             r = one_step()
-            samples += r["samples_drawn"]
+            samples += r["theta"]  # the sets the result uses (look-ahead may have drawn more)
             results.append(r)
         with torch.cuda.stream(stream):
             ev1.record(stream)
@@ -501,7 +501,7 @@ def run_ours(args, cfg, rank, world, local):
         if "lt_seed" in cfg:
             dge.set_lt_random(cfg["lt_seed"])
         r = im.run_device(dge, cfg["k"], **run_kw)  # results land in host memory
-        e2e_samples += r["samples_drawn"]
+        e2e_samples += r["theta"]
         del dge
     dev.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
@@ -553,7 +553,7 @@ def run_ours(args, cfg, rank, world, local):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
         "config": config_dict(args, cfg, world),
-        "theta": r0["theta"], "reuse_pool": True,
+        "theta": r0["theta"], "samples_drawn": r0["samples_drawn"], "reuse_pool": True,
         "imm_end_to_end_s": ms / args.steps / 1000.0,
         "step_ms": [round(x, 2) for x in step_ms],
         "compression_ratio": r0["compression_ratio"],

@@ -141,6 +141,26 @@ void estimate_theta_dev(const DevGraph& G, uint32_t k, double eps, uint64_t seed
     const uint64_t sampled_at_entry = sampled;
     double lower_bound = 0.0, last_fraction = -1.0;
     uint64_t theta_exit = 0;
+    // A first guess of the covered fraction, so iteration 1 can look ahead too: the fraction this graph's last estimation on this device ended with (same k), else
+    // the greedy's coverage of a 2,048-set pilot [0, 2048) -- the sets the sampler's own pilot
+    // batch would draw first anyway.  A greedy picked on few sets covers more of them than it
+    // would of many (it fits them), so the pilot errs towards less look-ahead.
+    Device& dev = *pool.dev;
+    const uint64_t kPilot = [] {  // IMMX_LA_PILOT=N: pilot of N sets (tests), 0 = neither guess
+        const char* e = std::getenv("IMMX_LA_PILOT");
+        return e && *e ? (uint64_t)std::strtoull(e, nullptr, 10) : (uint64_t)2048;
+    }();
+    if (la_margin > 0.0 && kPilot && i_max > 1) {
+        if (dev.seen_frac_graph == G.uid && dev.seen_frac_k == k && dev.seen_frac_eps == eps && dev.seen_frac >= 0.0) {
+            last_fraction = dev.seen_frac;
+        } else if (sampled == 0 && theta_of(1) >= 4 * kPilot && k < kPilot) {
+            sample_into_pool(pool, G, kPilot, 0, seed, nullptr, nullptr, model);
+            sampled = kPilot;
+            SelectOut sel;
+            select_raw_dev(pool, n, k, sel, kPilot);
+            last_fraction = sel.coverage.empty() ? -1.0 : sel.coverage.back();
+        }
+    }
     for (uint32_t i = 1; i <= i_max; ++i) {
         const uint64_t theta_i = theta_of(i);
         theta_exit = std::max(theta_exit, theta_i);
@@ -162,6 +182,10 @@ void estimate_theta_dev(const DevGraph& G, uint32_t k, double eps, uint64_t seed
         const double covered = sel.coverage.empty() ? 0.0 : sel.coverage.back();
         plan.covered_fraction = covered;
         last_fraction = covered;
+        dev.seen_frac_graph = G.uid;
+        dev.seen_frac_k = k;
+        dev.seen_frac_eps = eps;
+        dev.seen_frac = covered;
         const double x_i = (double)n / std::exp2((double)i);
         if ((double)n * covered >= (1.0 + eps_prime) * x_i) {
             plan.exit_iteration = i;

@@ -136,6 +136,11 @@ struct Device {
     // mean RRR set size last seen on a graph (sizes a cold pool's arena without a pilot batch)
     uint64_t seen_graph = 0;  // DevGraph::uid
     double seen_mean = 0.0;
+    // covered fraction the last theta estimation on a graph ended with (its next estimation's
+    // first look-ahead guess, capi.cu estimate_theta_dev)
+    uint64_t seen_frac_graph = 0;
+    uint32_t seen_frac_k = 0;
+    double seen_frac_eps = 0.0, seen_frac = -1.0;
 };
 
 // grow-only workspaces back to the allocator (end of immx_run: only the graph and the store

@@ -58,3 +58,32 @@ def test_forced_lookahead_draws_past_theta(im, orc, monkeypatch):
     r = im.run_device(dg, 5, epsilon=0.5, blocks=4, mode="huffman", seed=11)
     assert r["seeds"] == o["seeds"] and r["theta"] == o["theta"]
     assert r["samples_drawn"] >= r["theta"]
+
+
+@pytest.mark.parametrize("mode", ["raw", "huffman", "hybrid"])
+def test_pilot_and_remembered_fraction(im, orc, monkeypatch, mode):
+    """Iteration 1's look-ahead guess: a pilot's greedy coverage on a cold graph, the last
+    estimation's covered fraction on a graph this device has run before (same k, epsilon).
+    Both only choose how many sets a launch draws; plan and results stay the oracle's."""
+    monkeypatch.setenv("IMMX_LOOKAHEAD", "1.25")
+    monkeypatch.setenv("IMMX_LA_PILOT", "64")
+    rng = np.random.default_rng(31)
+    g = orc.assign_weights(random_graph(rng, 600, 6000), "wc")
+    o = orc.run(g, 5, 0.5, 4, mode, 13)
+    dg = im.DeviceGraph(to_product(im, g), transposed=False)
+    drawn = []
+    for rep in range(3):  # rep 0: pilot; rep 1, 2: the remembered fraction
+        r = im.run_device(dg, 5, epsilon=0.5, blocks=4, mode=mode, seed=13)
+        for key in ("seeds", "marginal", "coverage", "padded", "theta", "encoded_bytes", "peak_bytes"):
+            assert r[key] == o[key], (rep, key)
+        assert r["exit_iteration"] == o["exit_iteration"]
+        assert r["estimation_samples"] == o["estimation_samples"]
+        drawn.append(r["samples_drawn"])
+    assert drawn[1] == drawn[2]
+    # another k on the same graph: no remembered fraction for it, the pilot again
+    o2 = orc.run(g, 9, 0.5, 4, mode, 13)
+    r2 = im.run_device(dg, 9, epsilon=0.5, blocks=4, mode=mode, seed=13)
+    assert r2["seeds"] == o2["seeds"] and r2["theta"] == o2["theta"] and r2["coverage"] == o2["coverage"]
+    monkeypatch.setenv("IMMX_LA_PILOT", "0")
+    r3 = im.run_device(dg, 5, epsilon=0.5, blocks=4, mode=mode, seed=13)
+    assert r3["seeds"] == o["seeds"] and r3["theta"] == o["theta"]
