@@ -141,8 +141,10 @@ void estimate_theta_dev(const DevGraph& G, uint32_t k, double eps, uint64_t seed
     const uint64_t sampled_at_entry = sampled;
     double lower_bound = 0.0, last_fraction = -1.0;
     uint64_t theta_exit = 0;
-    // A first guess of the covered fraction, so iteration 1 can look ahead too: the fraction this graph's last estimation on this device ended with (same k), else
-    // the greedy's coverage of a 2,048-set pilot [0, 2048) -- the sets the sampler's own pilot
+    // A first guess of the covered fraction, so iteration 1 can look ahead too: the fraction
+    // the last estimation on this device ended with for this graph -- or for an upload of the
+    // same shape (n, m): a caller that sends its graph with every run -- and the same k and
+    // epsilon; else the greedy's coverage of a 2,048-set pilot [0, 2048) -- the sets the sampler's own pilot
     // batch would draw first anyway.  A greedy picked on few sets covers more of them than it
     // would of many (it fits them), so the pilot errs towards less look-ahead.
     Device& dev = *pool.dev;
@@ -151,7 +153,8 @@ void estimate_theta_dev(const DevGraph& G, uint32_t k, double eps, uint64_t seed
         return e && *e ? (uint64_t)std::strtoull(e, nullptr, 10) : (uint64_t)2048;
     }();
     if (la_margin > 0.0 && kPilot && i_max > 1) {
-        if (dev.seen_frac_graph == G.uid && dev.seen_frac_k == k && dev.seen_frac_eps == eps && dev.seen_frac >= 0.0) {
+        const bool same_graph = dev.seen_frac_graph == G.uid || (dev.seen_frac_n == G.n && dev.seen_frac_m == G.m);
+        if (same_graph && dev.seen_frac_k == k && dev.seen_frac_eps == eps && dev.seen_frac >= 0.0) {
             last_fraction = dev.seen_frac;
         } else if (sampled == 0 && theta_of(1) >= 4 * kPilot && k < kPilot) {
             sample_into_pool(pool, G, kPilot, 0, seed, nullptr, nullptr, model);
@@ -183,6 +186,8 @@ void estimate_theta_dev(const DevGraph& G, uint32_t k, double eps, uint64_t seed
         plan.covered_fraction = covered;
         last_fraction = covered;
         dev.seen_frac_graph = G.uid;
+        dev.seen_frac_n = G.n;
+        dev.seen_frac_m = G.m;
         dev.seen_frac_k = k;
         dev.seen_frac_eps = eps;
         dev.seen_frac = covered;

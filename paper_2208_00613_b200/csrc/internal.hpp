@@ -134,11 +134,15 @@ struct Device {
     std::shared_ptr<struct HostCodebook> run_cb;
     std::vector<unsigned long long> run_lut;
     // mean RRR set size last seen on a graph (sizes a cold pool's arena without a pilot batch)
+    // (both priors also apply to another upload of the same shape -- n and m -- e.g. a caller
+    // that sends its graph with every run: a wrong prior only costs a redo of the samples an
+    // undersized arena could not hold, or sets drawn past theta; no result depends on it)
     uint64_t seen_graph = 0;  // DevGraph::uid
+    uint64_t seen_n = 0, seen_m = 0;
     double seen_mean = 0.0;
     // covered fraction the last theta estimation on a graph ended with (its next estimation's
     // first look-ahead guess, capi.cu estimate_theta_dev)
-    uint64_t seen_frac_graph = 0;
+    uint64_t seen_frac_graph = 0, seen_frac_n = 0, seen_frac_m = 0;
     uint32_t seen_frac_k = 0;
     double seen_frac_eps = 0.0, seen_frac = -1.0;
 };
