@@ -44,6 +44,12 @@
 #ifndef IMMX_LONG_BITMAP
 #define IMMX_LONG_BITMAP 0  // 1: the long-row path in the bitmap tiers too (c2: 243 -> 226 Gedges/s)
 #endif
+#ifndef IMMX_COIN_MAX
+#define IMMX_COIN_MAX 1  // 1: long-row coins keep one running maximum per lane; 0: a success bit and a minimum per draw
+#endif
+#ifndef IMMX_COIN_U
+#define IMMX_COIN_U 4  // draws per early-exit check in the long-row coin loop (divides IMMX_LONG_LR)
+#endif
 #ifndef IMMX_LONG_LR
 #define IMMX_LONG_LR 16  // positions per thread per long-row slab (multiple of 4, <= 32)
 #endif
@@ -452,11 +458,19 @@ struct BHash {  // CTA-shared linear-probing hash (load <= 1/2) behind a one-has
     static constexpr uint32_t LOGF = LOGH + 3;
     static constexpr uint32_t FW = (1u << LOGF) / 32;
     __device__ static uint32_t h(uint32_t v) { return (v * 0x9E3779B1u) >> (32 - LOGH); }
-    __device__ static uint32_t fh(uint32_t v) { return (v * 0x85EBCA6Bu) >> (32 - LOGF); }
-    __device__ bool maybe(uint32_t v) const {
-        const uint32_t b = fh(v);
-        return (f[b >> 5] >> (b & 31)) & 1u;
+    // filter bit of a key, from one 64-bit product v * C: the word from the top LOGF-5 bits of
+    // its low half, the bit from the low 5 bits of its high half (bits 32..36 of the product
+    // -- the product's own low bits would only mix the key's low bits, and R-MAT ids repeat
+    // them).  The shift takes the bit index as it is: one instruction less per test than a
+    // contiguous LOGF-bit field.
+    __device__ static uint64_t fhash(uint32_t v) { return (uint64_t)v * 0x85EBCA6Bu; }
+    __device__ static uint32_t fword(uint64_t x) { return (uint32_t)x >> (32 - (LOGF - 5)); }
+    __device__ static uint32_t fbit(uint64_t x) { return (uint32_t)(x >> 32) & 31u; }
+    __device__ uint32_t maybe_raw(uint32_t v) const {  // bit 0: the key may be present
+        const uint64_t x = fhash(v);
+        return f[fword(x)] >> fbit(x);
     }
+    __device__ bool maybe(uint32_t v) const { return maybe_raw(v) & 1u; }
     __device__ bool probe(uint32_t v) const {
         uint32_t i = h(v);
         for (;;) {
@@ -468,8 +482,8 @@ struct BHash {  // CTA-shared linear-probing hash (load <= 1/2) behind a one-has
     }
     __device__ bool has(uint32_t v) const { return maybe(v) && probe(v); }
     __device__ bool add_test(uint32_t v) {
-        const uint32_t b = fh(v);
-        atomicOr(&f[b >> 5], 1u << (b & 31));
+        const uint64_t x = fhash(v);
+        atomicOr(&f[fword(x)], 1u << fbit(x));
         uint32_t i = h(v);
         for (;;) {
             const uint32_t old = atomicCAS(&s[i], kEmptyKey, v);
@@ -676,14 +690,14 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
             // long-row visited tests: a first, branch-free step (a filter bit where the set is a
             // hash or a promoted sample's global bitmap, else the exact bit), then the exact test
             constexpr bool kTwoStep = P || kHash;
-            auto lmaybe = [&](uint32_t v) -> bool {
+            auto lmaybe = [&](uint32_t v) -> uint32_t {  // bit 0 (the other bits are not defined)
                 if constexpr (P) {
                     const uint32_t b = pf_hash(v);
-                    return (dsm[b >> 5] >> (b & 31)) & 1u;
+                    return dsm[b >> 5] >> (b & 31);
                 } else if constexpr (kHash) {
-                    return vis.maybe(v);
+                    return vis.maybe_raw(v);
                 } else {
-                    return vis.has(v);
+                    return (uint32_t)vis.has(v);
                 }
             };
             auto lexact = [&](uint32_t v) -> bool {
@@ -754,8 +768,8 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                             // or the exact bit (bitmap tiers); the rare maybes re-read their target
                             uint32_t fm = 0;
     #pragma unroll
-                            for (int k = 0; k < (int)LR; ++k) fm |= (uint32_t)lmaybe(v[k]) << k;
-                            fm &= valid;
+                            for (int k = 0; k < (int)LR; ++k) fm = __funnelshift_r(fm, lmaybe(v[k]), 1);  // bit 0 in at the top
+                            fm = (fm >> (32 - LR)) & valid;
                             cm = valid & ~fm;
                             if constexpr (kTwoStep) {
                                 while (fm) {
@@ -820,9 +834,37 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                         const uint64_t z0 = s0 + d0 * kGamma;
                         const uint32_t nt = 1u - thi;
                         const uint32_t k4 = job.k4;
-                        uint32_t sr = 0, emin = (thi < 2u || job.exact_coins) ? 0u : FULL;
+                        uint32_t sr = 0;
                         const uint32_t nmax = __reduce_max_sync(__activemask(), nc);
                         uint64_t z = z0;
+    #if IMMX_COIN_MAX
+                        // One running maximum per lane: with e' = e - 3 (mod 2^32) a draw is a tie
+                        // iff e' >= 2^32 - 3 and a success iff nt - 3 <= e' < 2^32 - 3, so
+                        // "e' >= nt - 3" flags both (needs 2 <= thi <= 2^32 - 2).  Successes are
+                        // rare (a long row's p is ~1/degree): the lanes that saw one redo their
+                        // draws to find which -- no per-draw success bit in the common path.
+                        const uint32_t nt3 = nt - 3u;
+                        const bool force = thi < 2u || thi >= 0xfffffffeu || job.exact_coins;
+                        uint32_t emx = force ? FULL : 0u;
+    #pragma unroll
+                        for (uint32_t r0 = 0; r0 < LR; r0 += IMMX_COIN_U) {
+                            if (r0 >= nmax) break;  // (warp-uniform)
+    #pragma unroll
+                            for (uint32_t r = 0; r < IMMX_COIN_U; ++r) {
+                                emx = max(emx, IMMX_COIN_FMA ? zdiff_fma(z, nt3, k4) : zdiff_of(z, nt3));
+                                z += kGamma;
+                            }
+                        }
+                        if (emx >= nt3) {  // (draws past the lane's nc may flag it too: harmless)
+                            uint64_t z = z0;
+                            for (uint32_t r = 0; r < nc; ++r, z += kGamma) {
+                                const uint32_t e = zdiff_of(z, nt);
+                                const bool ok = (force || e < 3u) ? success_of(z, Trow) : e >= nt;
+                                sr |= (uint32_t)ok << r;
+                            }
+                        }
+    #else
+                        uint32_t emin = (thi < 2u || job.exact_coins) ? 0u : FULL;
     #pragma unroll
                         for (uint32_t r0 = 0; r0 < LR; r0 += 4) {
                             if (r0 >= nmax) break;  // (warp-uniform)
@@ -841,6 +883,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : (NW >= 16 ? 2 : (NW >=
                             uint64_t z = z0;
                             for (uint32_t r = 0; r < nc; ++r, z += kGamma) sr |= (uint32_t)success_of(z, Trow) << r;
                         }
+    #endif
                         // rank -> position (rare)
                         while (sr) {
                             const uint32_t r = __ffs(sr) - 1;
@@ -1453,7 +1496,7 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     if (G.n == 0) fail(IMMX_EINVAL, "graph has no vertices");
     if (model == IMMX_MODEL_LT && !G.has_lt) fail(IMMX_EINVAL, "LT model requires per-edge LT weights");
     // mean set size: the pool's, else the last one seen on this graph on this device
-    const bool known = d.seen_graph == G.uid && d.seen_mean > 0.0;
+    const bool known = (d.seen_graph == G.uid || (d.seen_n == G.n && d.seen_m == G.m)) && d.seen_mean > 0.0;
     if (P.count < 1024 && count > 8192 && !known) {
         // cold pool on a new graph: a pilot batch measures the mean set size, so the arena is
         // sized once (an undersized arena makes in-flight samples redo their work); repeated
@@ -1692,6 +1735,8 @@ void sample_into_pool(Pool& P, const DevGraph& G, uint64_t count, uint64_t first
     P.edges += edges;
     if (P.count >= 1024) {
         d.seen_graph = G.uid;
+        d.seen_n = G.n;
+        d.seen_m = G.m;
         d.seen_mean = (double)P.members / (double)P.count;
     }
 }
