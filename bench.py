@@ -554,6 +554,9 @@ def run_ours(args, cfg, rank, world, local):
         "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
         "config": config_dict(args, cfg, world),
         "theta": r0["theta"], "samples_drawn": r0["samples_drawn"], "reuse_pool": True,
+        "scheduling_priors": "the timed steps run with the mean set size (arena sizing) and the covered fraction "
+                             "(look-ahead sampling) the device remembered from the warm-up steps on this graph shape; "
+                             "they choose launch sizes only, every result is the reference's (DESIGN.md section 2)",
         "imm_end_to_end_s": ms / args.steps / 1000.0,
         "step_ms": [round(x, 2) for x in step_ms],
         "compression_ratio": r0["compression_ratio"],
