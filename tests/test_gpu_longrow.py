@@ -18,7 +18,11 @@ def long_min(request, monkeypatch):
 
 
 @pytest.mark.parametrize("model,p", [("wc", 0.0), ("uniform", 0.1), ("uniform", 0.5), ("uniform", 1.0),
-                                     ("uniform", 0.0)])
+                                     ("uniform", 0.0),
+                                     # thresholds whose high word is outside [2, 2^32 - 2]: the coin
+                                     # loop's running maximum cannot flag them, every draw goes
+                                     # through the full 64-bit test
+                                     ("uniform", 1.0 - 1e-12), ("uniform", 1e-12), ("uniform", 3e-10)])
 def test_long_rows_random_graphs(im, orc, long_min, model, p):
     rng = np.random.default_rng(21)
     for trial in range(4):
