@@ -427,11 +427,16 @@ def run_ours(args, cfg, rank, world, local):
         return im.run_device(dg, cfg["k"], **run_kw)
 
     tw = time.perf_counter()
+    warm_ms = []  # wall time per warm-up step; the first runs on a graph the device has not seen
     for _ in range(args.warmup):
         with torch.cuda.stream(stream):
             flush.fill_(1)  # (warms the flush kernel too: its first launch loads the module, ~40 ms)
             torch.cuda.Event(enable_timing=True).record(stream)
+        dev.synchronize()
+        t1 = time.perf_counter()
         one_step()
+        dev.synchronize()
+        warm_ms.append(round((time.perf_counter() - t1) * 1e3, 2))
     dev.synchronize()
     # clocks polled once a second in regions >= 2 s, else right after the region (an
     # nvidia-smi query could stall the driver for tens of ms; NVML is polled in-process)
@@ -559,6 +564,7 @@ def run_ours(args, cfg, rank, world, local):
                              "they choose launch sizes only, every result is the reference's (DESIGN.md section 2)",
         "imm_end_to_end_s": ms / args.steps / 1000.0,
         "step_ms": [round(x, 2) for x in step_ms],
+        "warmup_step_ms": warm_ms,  # [0]: no scheduling priors yet (and one-time costs: module load, pool growth)
         "compression_ratio": r0["compression_ratio"],
         "dense_sets": r0.get("dense_sets", 0),
         "compression_ratio_device": r0["raw_bytes"] / r0["device_store_bytes"] if r0["device_store_bytes"] else None,
