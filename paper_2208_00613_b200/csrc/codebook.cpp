@@ -36,13 +36,19 @@ void merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id, bool per_verte
     if (!L) fail(IMMX_ERUNTIME, "cannot build a codebook from an empty block");
     if (L >= (1ULL << 31)) fail(IMMX_EINVAL, "too many coded symbols");
     cb.coded = L;
-    cb.nodes.assign(L == 1 ? 2 : 2 * L - 1, HostCodebook::Node{});
-    for (uint64_t i = 0; i < L; ++i) cb.nodes[i].symbol = leaf_id(i);
+    // (every node is written below -- leaves here, merged nodes by the merge loop -- so the
+    // array is only resized: no 68 MB value-initialisation pass on a c5-sized alphabet)
+    cb.nodes.resize(L == 1 ? 2 : 2 * L - 1);
+    cb.leaf_sym.resize(L);
+    for (uint64_t i = 0; i < L; ++i) {
+        const uint32_t id = leaf_id(i);
+        cb.nodes[i] = HostCodebook::Node{{-1, -1}, id};
+        cb.leaf_sym[i] = id;
+    }
     if (L == 1) {
-        cb.nodes[1].child[0] = 0;
+        cb.nodes[1] = HostCodebook::Node{{0, -1}, 0};
         cb.root = 1;
         // a single symbol gets the 1-bit code "0"
-        cb.leaf_sym.assign(1, leaf_id(0));
         cb.leaf_bits.assign(1, 0);
         cb.leaf_len.assign(1, 1);
         if (per_vertex) {
@@ -88,32 +94,42 @@ void merge_sorted(uint64_t L, uint64_t n, F leaf_freq, I leaf_id, bool per_verte
         const int32_t a = pop(fa, ma);  // first popped: branch 0
         const int32_t b = pop(fb, mb);
         const int32_t u = (int32_t)(L + k);
-        cb.nodes[u].child[0] = a;
-        cb.nodes[u].child[1] = b;
+        cb.nodes[u] = HostCodebook::Node{{a, b}, 0};
         q.push_back({fa + fb, std::min(ma, mb), u});
     }
     cb.root = (int32_t)(2 * L - 2);
-    // codes top-down: parents come after their children, so walk the merged nodes backwards
+    // codes top-down: parents come after their children, so walk the merged nodes backwards.
+    // Prefix and depth are kept for the merged nodes only (index u - L; the root's are 0 and
+    // every other entry is written by its parent before it is read); a leaf's go straight into
+    // the per-leaf outputs.
     static thread_local std::vector<uint64_t> pre;
     static thread_local std::vector<uint8_t> dep;
-    pre.assign(cb.nodes.size(), 0);
-    dep.assign(cb.nodes.size(), 0);
+    if (pre.size() < L) pre.resize(L);
+    if (dep.size() < L) dep.resize(L);
+    cb.leaf_bits.resize(L);
+    cb.leaf_len.resize(L);
+    pre[cb.root - L] = 0;
+    dep[cb.root - L] = 0;
     for (int64_t u = cb.root; u >= (int64_t)L; --u) {
-        if (dep[u] >= 64) fail(IMMX_ERUNTIME, "huffman code longer than 64 bits");
+        const uint64_t pu = pre[u - L];
+        const uint8_t du = dep[u - L];
+        if (du >= 64) fail(IMMX_ERUNTIME, "huffman code longer than 64 bits");
         for (int c = 0; c < 2; ++c) {
             const int32_t ch = cb.nodes[u].child[c];
-            pre[ch] = (pre[u] << 1) | (uint64_t)c;
-            dep[ch] = (uint8_t)(dep[u] + 1);
+            const uint64_t pc = (pu << 1) | (uint64_t)c;
+            if ((uint64_t)ch < L) {
+                cb.leaf_bits[ch] = pc;
+                cb.leaf_len[ch] = (uint8_t)(du + 1);
+            } else {
+                pre[ch - L] = pc;
+                dep[ch - L] = (uint8_t)(du + 1);
+            }
         }
     }
-    cb.leaf_sym.resize(L);
-    cb.leaf_bits.assign(pre.begin(), pre.begin() + L);
-    cb.leaf_len.assign(dep.begin(), dep.begin() + L);
-    for (uint64_t i = 0; i < L; ++i) cb.leaf_sym[i] = cb.nodes[i].symbol;
     if (per_vertex)
         for (uint64_t i = 0; i < L; ++i) {
-            cb.bits[cb.nodes[i].symbol] = pre[i];
-            cb.len[cb.nodes[i].symbol] = dep[i];
+            cb.bits[cb.leaf_sym[i]] = cb.leaf_bits[i];
+            cb.len[cb.leaf_sym[i]] = cb.leaf_len[i];
         }
 }
 
