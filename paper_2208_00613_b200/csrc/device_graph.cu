@@ -12,6 +12,10 @@
 
 #include <vector>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "internal.hpp"
 
 namespace immx_dev {
@@ -58,6 +62,8 @@ __global__ void k_row_scan(const uint64_t* __restrict__ row, const uint32_t* __r
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t wmax = 0;  // the warp's longest row: one atomic per warp, not one per row (on config
+                        // 5's 33.5 M rows the same-address atomics were ~50 ms of a 157 ms upload)
     for (uint64_t v = w; v < n; v += nw) {
         const uint64_t b = row[v], e = row[v + 1];
         if (b == e) {
@@ -76,9 +82,10 @@ __global__ void k_row_scan(const uint64_t* __restrict__ row, const uint32_t* __r
             rthr[v] = (T == kThrNever || T == kThrAlways) ? T : (T << 11);
             unsigned int f = (fm ? 1u : 0u) | (fu ? 2u : 0u);
             if (f) atomicOr(flags, f);
-            atomicMax(maxdeg, (uint32_t)(e - b));
+            wmax = max(wmax, (uint32_t)(e - b));
         }
     }
+    if (lane == 0 && wmax) atomicMax(maxdeg, wmax);
 }
 
 __global__ void k_edge_thr(const double* __restrict__ prob, uint64_t m, uint64_t* __restrict__ thr) {
@@ -91,10 +98,52 @@ __global__ void k_edge_thr(const double* __restrict__ prob, uint64_t m, uint64_t
 // are all non-empty rows' thresholds equal? (min/max over rows with edges)
 __global__ void k_row_minmax(const uint64_t* __restrict__ row, const uint64_t* __restrict__ rthr, uint64_t n,
                              unsigned long long* __restrict__ mn, unsigned long long* __restrict__ mx) {
+    // (one atomic pair per warp: one per row serialised 2 x 20 M same-address atomics on config 5)
+    unsigned long long lo = ~0ULL, hi = 0ULL;
+    bool any = false;
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
         if (row[v] == row[v + 1]) continue;
-        atomicMin(mn, (unsigned long long)rthr[v]);
-        atomicMax(mx, (unsigned long long)rthr[v]);
+        const unsigned long long t = rthr[v];
+        lo = min(lo, t);
+        hi = max(hi, t);
+        any = true;
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, (unsigned long long)__shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, (unsigned long long)__shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) {
+        atomicMin(mn, lo);
+        atomicMax(mx, hi);
+    }
+}
+
+// The row scan of a model-weighted upload (no per-edge probabilities): only "is some row not
+// strictly increasing" and the longest row are needed, and both stream.  Descents
+// col[i] >= col[i+1] are counted over ALL adjacent edge pairs (edge-parallel) and over the pairs
+// that straddle two rows (row-parallel, with the longest row); a row is unsorted iff the counts
+// differ.  (The warp-per-row scan below took 26 ms on config 5's 33.5 M rows.)
+__global__ void k_edge_descents(const uint32_t* __restrict__ col, uint64_t m, unsigned long long* __restrict__ all) {
+    unsigned int c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < m; i += (uint64_t)gridDim.x * blockDim.x)
+        c += col[i] >= col[i + 1];
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(all, (unsigned long long)c);
+}
+__global__ void k_row_bounds(const uint64_t* __restrict__ row, const uint32_t* __restrict__ col, uint64_t n, uint64_t m,
+                             unsigned long long* __restrict__ straddling, uint32_t* __restrict__ maxdeg) {
+    unsigned int c = 0, dmax = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = row[v], e = row[v + 1];
+        if (b == e) continue;
+        dmax = max(dmax, (uint32_t)(e - b));
+        if (e < m) c += col[e - 1] >= col[e];  // this row's last edge against the next row's first
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    dmax = __reduce_max_sync(0xffffffffu, dmax);
+    if ((threadIdx.x & 31) == 0) {
+        if (c) atomicAdd(straddling, (unsigned long long)c);
+        if (dmax) atomicMax(maxdeg, dmax);
     }
 }
 
@@ -157,6 +206,16 @@ unsigned grid_for(uint64_t items, const Device& d, unsigned per_thread = 1) {
 void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t* off, const uint32_t* tgt,
                   const double* prob, bool transposed, int weight_model, double wp) {
     cudaStream_t s = d.stream;
+    // IMMX_DEBUG_UPLOAD=1: host time per phase on stderr (each mark synchronises the stream)
+    const bool dbg = std::getenv("IMMX_DEBUG_UPLOAD") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!dbg) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[immx upload] %s %.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_prev).count());
+        t_prev = now;
+    };
     if (n == 0) fail(IMMX_EINVAL, "graph has no vertices");
     if (n >= 0xffffffffULL) fail(IMMX_EINVAL, "vertex ids are 32-bit");
     if (m >= 0xffffffffULL) fail(IMMX_EINVAL, "edge count must be < 2^32");
@@ -172,6 +231,7 @@ void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t
     const bool by_model = prob == nullptr;
     DBuf<double> dprob;
     if (!by_model) dprob.exact(std::max<uint64_t>(m, 1));
+    mark("alloc");
     if (transposed) {
         CK(cudaMemcpyAsync(G.row.p, off, (n + 1) * 8, cudaMemcpyHostToDevice, s));
         if (m) CK(cudaMemcpyAsync(G.col.p, tgt, m * 4, cudaMemcpyHostToDevice, s));
@@ -220,19 +280,34 @@ void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t
         CK(cub::DeviceScan::InclusiveSum(d.tmp.p, tmp_bytes, cnt.p, (unsigned long long*)G.row.p, n + 1, s));
         CK(cudaStreamSynchronize(s));  // temporaries die at scope end
     }
+    mark("copy / transpose");
     // thresholds
     DBuf<uint64_t> rthr;
     rthr.exact(n);
     DBuf<unsigned int> flags;
     flags.exact(4);
     CK(cudaMemsetAsync(flags.p, 0, 16, s));
-    k_row_scan<<<grid_for(n * 32, d), 256, 0, s>>>(G.row.p, G.col.p, dprob.p, n, rthr.p, flags.p, flags.p + 1);
-    d.kernel_launches++;
     unsigned int hflags[2] = {0, 0};
-    CK(cudaMemcpyAsync(hflags, flags.p, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if (by_model) {
+        unsigned long long* cnt = d.scal.p + 2;  // [2] = all descents, [3] = row-straddling descents
+        CK(cudaMemsetAsync(cnt, 0, 16, s));
+        if (m > 1) k_edge_descents<<<grid_for(m, d), 256, 0, s>>>(G.col.p, m, cnt);
+        k_row_bounds<<<grid_for(n, d), 256, 0, s>>>(G.row.p, G.col.p, n, m, cnt + 1, flags.p + 1);
+        d.kernel_launches += 2;
+        unsigned long long hc[2] = {0, 0};
+        CK(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hflags, flags.p, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        hflags[0] = hc[0] != hc[1] ? 2u : 0u;  // (no per-edge probabilities: never "mixed")
+    } else {
+        k_row_scan<<<grid_for(n * 32, d), 256, 0, s>>>(G.row.p, G.col.p, dprob.p, n, rthr.p, flags.p, flags.p + 1);
+        d.kernel_launches++;
+        CK(cudaMemcpyAsync(hflags, flags.p, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
     G.row_dups = (hflags[0] & 2u) != 0;
     G.max_deg = hflags[1];
+    mark("row scan");
     if (by_model) {
         k_model_row_thr<<<grid_for(n, d), 256, 0, s>>>(G.row.p, n, weight_model, (double)(float)wp, rthr.p);
         d.kernel_launches++;
@@ -263,6 +338,7 @@ void graph_upload(DevGraph& G, Device& d, uint64_t n, uint64_t m, const uint64_t
         }
     }
     CK(cudaStreamSynchronize(s));
+    mark("thresholds");
 }
 
 void graph_set_lt(DevGraph& G, const float* w) {
